@@ -1,0 +1,239 @@
+"""Float64 CPU oracle for GGX VNDF spherical-cap sampling (arXiv 2306.05044).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py`` (its ``cpu_baseline`` leg and ``--impl reference``) may import
+this package.  It shares no code with the CUDA path in
+``paper_2306_05044_b200/`` and never imports it.
+
+The arithmetic lives in ``oracle.c`` (plain C, float64, every function cites
+the PAPER.md passage it follows); this module only loads it with ctypes and
+marshals numpy arrays.  ``stats.py`` holds the chi-square / quadrature
+machinery used by the distributional tests.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+# Plain scalar float64 build: -O2, no -ffast-math, no vectorisation tricks
+# that could change rounding (-ffp-contract=off keeps a*b+c as two roundings
+# unless the source calls fma() explicitly, as Listing 3 line 6 does).
+CFLAGS = ["-O2", "-std=c11", "-fPIC", "-shared", "-pthread", "-ffp-contract=off"]
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c into liboracle.so (gcc).  Returns the library path."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["gcc", *CFLAGS, _SRC, "-o", _LIB, "-lm"]
+        subprocess.run(cmd, check=True)
+    return _LIB
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        d, u32, u64, i64, i32 = (ctypes.c_double, ctypes.c_uint32, ctypes.c_uint64,
+                                  ctypes.c_int64, ctypes.c_int)
+        P = ctypes.c_void_p
+        L.orc_philox4x32_10.argtypes = [P, P, P]
+        L.orc_philox_block.argtypes = [u64, u64, u32, P]
+        L.orc_u01.argtypes = [u32]
+        L.orc_u01.restype = d
+        L.orc_sample_vndf.argtypes = [i32, P, d, d, d, d, P, P]
+        L.orc_sample_hemisphere.argtypes = [i32, d, d, P, P]
+        for name in ("orc_sigma_std", "orc_D_std"):
+            getattr(L, name).argtypes = [d]
+            getattr(L, name).restype = d
+        L.orc_Dvis_std.argtypes = [P, P]
+        L.orc_Dvis_std.restype = d
+        for name in ("orc_pdf_vndf", "orc_pdf_vndf_g1d", "orc_G1"):
+            getattr(L, name).argtypes = [P, P, d, d]
+            getattr(L, name).restype = d
+        L.orc_D_ggx.argtypes = [P, d, d]
+        L.orc_D_ggx.restype = d
+        L.orc_reflect.argtypes = [P, P, P]
+        L.orc_half_vector.argtypes = [P, P, P]
+        L.orc_reflect_jacobian.argtypes = [P, P]
+        L.orc_reflect_jacobian.restype = d
+        L.orc_cap_density.argtypes = [P, P]
+        L.orc_cap_density.restype = d
+        L.orc_sample_raycast.argtypes = [P, d, d, u64, u64, P]
+        L.orc_sample_raycast.restype = u64
+        L.orc_c4_inputs.argtypes = [u64, u64, P]
+        L.orc_batch_sample.argtypes = [i32, i64] + [P] * 7 + [P] * 5 + [i32]
+        L.orc_batch_sample_philox.argtypes = [i32, u64, i64, P] + [P] * 5 + [i32]
+        L.orc_batch_pdf.argtypes = [i64] + [P] * 9
+        L.orc_batch_philox_words.argtypes = [u64, i64, P, u32, P]
+        L.orc_batch_raycast.argtypes = [P, d, d, u64, i64, P, P, P]
+        L.orc_batch_raycast.restype = u64
+        _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray) -> ctypes.c_void_p:
+    # data_as keeps a reference to `a`, so temporaries outlive the C call
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _vec(v) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(v, dtype=np.float64).reshape(3))
+
+
+def default_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------- Philox ---
+def philox4x32_10(ctr, key) -> np.ndarray:
+    c = np.ascontiguousarray(np.asarray(ctr, dtype=np.uint32).reshape(4))
+    k = np.ascontiguousarray(np.asarray(key, dtype=np.uint32).reshape(2))
+    out = np.zeros(4, dtype=np.uint32)
+    lib().orc_philox4x32_10(_p(c), _p(k), _p(out))
+    return out
+
+
+def philox_words(seed: int, indices, block: int) -> np.ndarray:
+    idx = np.ascontiguousarray(np.asarray(indices, dtype=np.uint64).reshape(-1))
+    out = np.zeros((idx.size, 4), dtype=np.uint32)
+    lib().orc_batch_philox_words(seed, idx.size, _p(idx), block, _p(out))
+    return out
+
+
+def u01(word: int) -> float:
+    return lib().orc_u01(word)
+
+
+def c4_inputs(seed: int, index: int) -> np.ndarray:
+    out = np.zeros(7, dtype=np.float64)
+    lib().orc_c4_inputs(seed, index, _p(out))
+    return out
+
+
+# --------------------------------------------------------------- scalars ---
+CAP, HEITZ = 0, 1
+
+
+def sample_vndf(method: int, wi, ax: float, ay: float, u1: float, u2: float):
+    """Listing 1 + Listing 3 (method CAP) or Listing 2 (HEITZ); float64."""
+    w = _vec(wi)
+    h = np.zeros(3)
+    ti = np.zeros(1)
+    lib().orc_sample_vndf(method, _p(w), ax, ay, u1, u2, _p(h), _p(ti))
+    return h
+
+
+def sample_hemisphere(method: int, u1: float, u2: float, wi) -> np.ndarray:
+    """Listing 3 (unnormalised c + wi) or Listing 2 alone; native, no flip."""
+    h = np.zeros(3)
+    lib().orc_sample_hemisphere(method, u1, u2, _p(_vec(wi)), _p(h))
+    return h
+
+
+def pdf_vndf(h, wi, ax, ay) -> float:
+    return lib().orc_pdf_vndf(_p(_vec(h)), _p(_vec(wi)), ax, ay)
+
+
+def pdf_vndf_g1d(h, wi, ax, ay) -> float:
+    return lib().orc_pdf_vndf_g1d(_p(_vec(h)), _p(_vec(wi)), ax, ay)
+
+
+def D_ggx(h, ax, ay) -> float:
+    return lib().orc_D_ggx(_p(_vec(h)), ax, ay)
+
+
+def G1(h, wi, ax, ay) -> float:
+    return lib().orc_G1(_p(_vec(h)), _p(_vec(wi)), ax, ay)
+
+
+def sigma_std(zi: float) -> float:
+    return lib().orc_sigma_std(zi)
+
+
+def D_std(zm: float) -> float:
+    return lib().orc_D_std(zm)
+
+
+def Dvis_std(wm, wi) -> float:
+    return lib().orc_Dvis_std(_p(_vec(wm)), _p(_vec(wi)))
+
+
+def reflect(wi, wm) -> np.ndarray:
+    out = np.zeros(3)
+    lib().orc_reflect(_p(_vec(wi)), _p(_vec(wm)), _p(out))
+    return out
+
+
+def half_vector(wi, wo) -> np.ndarray:
+    out = np.zeros(3)
+    lib().orc_half_vector(_p(_vec(wi)), _p(_vec(wo)), _p(out))
+    return out
+
+
+def reflect_jacobian(wo, wh) -> float:
+    return lib().orc_reflect_jacobian(_p(_vec(wo)), _p(_vec(wh)))
+
+
+def cap_density(wo, wi) -> float:
+    return lib().orc_cap_density(_p(_vec(wo)), _p(_vec(wi)))
+
+
+# --------------------------------------------------------------- batches ---
+def batch_sample(method: int, wx, wy, wz, ax, ay, u1, u2, *, pdf: bool = True,
+                 threads: int | None = None):
+    """Oracle over fp32 SoA planes.  Returns (h[3,n] float64, pdf[n] or None, aux[n])."""
+    planes = [np.ascontiguousarray(np.asarray(a, dtype=np.float32).reshape(-1))
+              for a in (wx, wy, wz, ax, ay, u1, u2)]
+    n = planes[0].size
+    h = np.empty((3, n), dtype=np.float64)
+    p = np.empty(n, dtype=np.float64) if pdf else None
+    aux = np.empty(n, dtype=np.float64)
+    lib().orc_batch_sample(method, n, *[_p(a) for a in planes],
+                           _p(h[0]), _p(h[1]), _p(h[2]),
+                           _p(p) if pdf else None, _p(aux),
+                           threads or default_threads())
+    return h, p, aux
+
+
+def batch_sample_philox(method: int, seed: int, indices, *, threads: int | None = None):
+    idx = np.ascontiguousarray(np.asarray(indices, dtype=np.uint64).reshape(-1))
+    n = idx.size
+    h = np.empty((3, n), dtype=np.float64)
+    p = np.empty(n, dtype=np.float64)
+    aux = np.empty(n, dtype=np.float64)
+    lib().orc_batch_sample_philox(method, seed, n, _p(idx), _p(h[0]), _p(h[1]), _p(h[2]),
+                                  _p(p), _p(aux), threads or default_threads())
+    return h, p, aux
+
+
+def batch_pdf(h, wi, ax, ay) -> np.ndarray:
+    h = np.ascontiguousarray(np.asarray(h, dtype=np.float64).reshape(3, -1))
+    wi = np.ascontiguousarray(np.asarray(wi, dtype=np.float64).reshape(3, -1))
+    n = h.shape[1]
+    ax = np.ascontiguousarray(np.broadcast_to(np.asarray(ax, dtype=np.float64), (n,)))
+    ay = np.ascontiguousarray(np.broadcast_to(np.asarray(ay, dtype=np.float64), (n,)))
+    out = np.empty(n, dtype=np.float64)
+    lib().orc_batch_pdf(n, _p(h[0]), _p(h[1]), _p(h[2]), _p(wi[0]), _p(wi[1]), _p(wi[2]),
+                        _p(ax), _p(ay), _p(out))
+    return out
+
+
+def batch_raycast(wi, ax, ay, seed: int, n: int):
+    """Brute-force ray-cast VNDF samples (definition). Returns (h[3,n], trials)."""
+    h = np.empty((3, n), dtype=np.float64)
+    trials = lib().orc_batch_raycast(_p(_vec(wi)), ax, ay, seed, n, _p(h[0]), _p(h[1]), _p(h[2]))
+    return h, trials
