@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of GGX VNDF spherical-cap sampling on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step is one pass of the hot path (DESIGN.md s.2: stretch, cap sample, half
+vector, unstretch, pdf, float64 fix-up of flagged samples) over one batch of
+BASELINE.json configs[1] (config 2: 2^24 samples, wi cosine-weighted, alpha
+log-uniform [0.01, 1], h + pdf), i.e. ONE launch of vndf_sample_cap_pdf.
+Inputs (28 B/sample, 470 MB) and outputs (16 B/sample) exceed the 126 MB L2,
+so no flush is needed between steps.  Under torchrun each rank processes its
+own batch (global indices rank*n ...): weak scaling, no data-path collective.
+
+Prints ONE JSON line on rank 0.  `value` is whole-job Gsamples/s timed with
+CUDA events on the launching stream, max over ranks; `e2e` is the same metric
+through the blocking host-buffer entry point vndf_sample_cap_pdf_host with
+pinned host memory (copies inside the timed region); `roofline` is for the
+dominant kernel; `cpu_baseline` is the float64 oracle on this box's cores.
+`--impl reference` times the oracle itself (the tier's reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "Gsamples/s of GGX VNDF spherical-cap sampling; % HBM/FP32 roofline; vs Heitz18"
+UNIT = "Gsamples/s"
+WORKLOAD_CID = 2
+BYTES_PER_SAMPLE = {True: 44, False: 40}   # 28 B in + 16 B (h + pdf) or 12 B (h) out
+FALLBACK_HBM_GBS = 6650.0                   # B200_PROFILING.md fallback, if MEASURED_PEAKS.json is absent
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--no-variants", action="store_true", help="skip the config 3/4/5 and Heitz side runs")
+    p.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline leg")
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            mp = json.load(f)
+        return float(mp["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)", mp
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)", {}
+
+
+def profiled_traffic(kernel_key: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed
+    ncu --set full summary (profiles/traffic.json), else None."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(kernel_key)
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------- clocks ---
+class ClockSampler:
+    """Polls NVML SM clock and clock-event reasons during the timed region."""
+
+    BAD = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown")
+
+    def __init__(self, index: int, period_s: float = 0.005):
+        self.index, self.period = index, period_s
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._nv = None
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self._nv = nv
+            self._h = nv.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+
+    def _poll(self):
+        nv = self._nv
+        try:
+            self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            names = {nv.nvmlClocksEventReasonHwSlowdown: "hw_slowdown",
+                     nv.nvmlClocksEventReasonHwThermalSlowdown: "hw_thermal_slowdown",
+                     nv.nvmlClocksEventReasonSwThermalSlowdown: "sw_thermal_slowdown",
+                     nv.nvmlClocksEventReasonSwPowerCap: "sw_power_cap",
+                     nv.nvmlClocksEventReasonHwPowerBrakeSlowdown: "hw_power_brake_slowdown"}
+            for bit, nm in names.items():
+                if r & bit:
+                    self.reasons.add(nm)
+        except Exception:
+            pass
+
+    def _run(self):
+        while not self._stop.is_set():
+            self._poll()
+            time.sleep(self.period)
+
+    def start(self):
+        if self._nv is None:
+            return
+        self._poll()
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        if self._nv is None:
+            return
+        self._stop.set()
+        self._t.join()
+        self._poll()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        s = sorted(self.samples)
+        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "n_samples": len(s)}
+
+
+# ------------------------------------------------------------ timed loops ---
+def time_launches(torch, fn, steps: int, warmup: int, stream, barrier=None):
+    """W untimed warm-up launches, then `steps` launches bracketed by events on
+    `stream`.  Returns (total_ms, per_launch_ms list)."""
+    for _ in range(warmup):
+        fn()
+    if barrier:
+        barrier()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    ev[0].record(stream)
+    for k in range(steps):
+        fn()
+        ev[k + 1].record(stream)
+    torch.cuda.synchronize()
+    per = [ev[k].elapsed_time(ev[k + 1]) for k in range(steps)]
+    return ev[0].elapsed_time(ev[steps]), per
+
+
+def cpu_baseline(host_planes, n_sample: int, budget_s: float = 12.0):
+    """The float64 oracle, as it stands, on this box's host cores, on a bounded
+    sample (the first n_sample samples of the workload, repeated until ~budget_s)."""
+    import oracle
+    import numpy as np
+    threads = oracle.default_threads()
+    planes = [np.ascontiguousarray(p[:n_sample]) for p in host_planes]
+    done, t0 = 0, time.perf_counter()
+    while True:
+        oracle.batch_sample(oracle.CAP, *planes, pdf=True, threads=threads)
+        done += n_sample
+        if time.perf_counter() - t0 >= budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": done / dt / 1e9, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"first {n_sample} samples of config 2 (float64 Listing 1+3 + Eq. 1 pdf), "
+                      f"{done // n_sample} passes in {dt:.1f} s, {threads} threads"}
+
+
+def roofline(bytes_per_launch: float, launch_ms: float, kernel_key: str):
+    peak, src, _ = peaks()
+    achieved = bytes_per_launch / (launch_ms * 1e-3) / 1e9
+    return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": profiled_traffic(kernel_key),
+            "peak_source": src, "kernel": kernel_key,
+            "algorithmic_bytes_per_launch": int(bytes_per_launch)}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_2306_05044_b200 as vndf
+    import synth
+
+    cfg = synth.CONFIGS[WORKLOAD_CID]
+    n = cfg.n
+    stream = torch.cuda.current_stream(dev)
+    # weak scaling: rank r owns global samples [r n, (r + 1) n)
+    x = synth.fill(cfg.recipe, cfg.seed, n, first=rank * n, device=dev)
+    ins = [x[k] for k in synth.PLANES]
+    out = vndf.empty_outputs(n, dev, pdf=True)
+    torch.cuda.synchronize()
+
+    def step():
+        vndf.vndf_sample_cap_pdf(*ins, *out, n=n, stream=stream)
+
+    barrier = (lambda: dist.barrier()) if world > 1 else None
+    clocks = ClockSampler(dev.index if world == 1 else local)
+    for _ in range(args.warmup):
+        step()
+    if barrier:
+        barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    total_ms, per = time_launches(torch, step, args.steps, 0, stream)
+    clocks.stop()
+    if barrier:
+        barrier()
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = world * n * args.steps / (total_ms * 1e-3) / 1e9
+
+    # ---- end to end: host buffers through the public host entry point ----
+    e2e_steps = max(1, min(args.steps, 10))
+    hin = [p.cpu().pin_memory() for p in ins]
+    hout = [torch.empty(n, dtype=torch.float32).pin_memory() for _ in range(4)]
+    vndf.vndf_sample_cap_pdf_host(*hin, *hout, n=n)          # warm-up
+    if barrier:
+        barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        vndf.vndf_sample_cap_pdf_host(*hin, *hout, n=n)
+    e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e = {"value": world * n * e2e_steps / float(te.item()) / 1e9, "unit": UNIT,
+           "h2d_bytes_per_step": 28 * n, "d2h_bytes_per_step": 16 * n,
+           "api": "vndf_sample_cap_pdf_host (pinned host buffers, blocking)"}
+
+    result = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded counter-based Philox recipe, DESIGN.md s.5)",
+        "config": {"workload": f"config 2: {cfg.label}", "samples_per_gpu_per_step": n,
+                   "kernel": "vndf_sample_cap_pdf", "parallelism": f"independent shards x{world}",
+                   "l2": "inputs 470 MB + outputs 268 MB per step > 126 MB L2; no flush"},
+        "roofline": roofline(BYTES_PER_SAMPLE[True] * n, ms_per_step, "cap_pdf_c2"),
+        "clocks": clocks.summary(),
+        "e2e": e2e,
+        "gpu_launches": args.steps,
+    }
+
+    if world == 1 and not args.no_variants:
+        result["variants"] = variants(torch, vndf, synth, dev, stream, x, out)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        host = [p.cpu().numpy() for p in ins]
+        result["cpu_baseline"] = cpu_baseline(host, 1 << 22)
+    elif rank == 0:
+        result["cpu_baseline"] = None
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def variants(torch, vndf, synth, dev, stream, x2, out2):
+    """Side measurements on identical inputs (not the headline): Heitz-2018 on
+    config 2, configs 3/4/5 (cap and Heitz), each 3 warm-up + 10 timed launches."""
+    res = {}
+    reps, warm = 10, 3
+
+    def timed(fn):
+        total, per = time_launches(torch, fn, reps, warm, stream)
+        return total / reps
+
+    n2 = x2["wi_x"].numel()
+    ins2 = [x2[k] for k in synth.PLANES]
+    t_cap = timed(lambda: vndf.vndf_sample_cap_pdf(*ins2, *out2, stream=stream))
+    t_hz = timed(lambda: vndf.vndf_sample_heitz2018(*ins2, *out2, stream=stream))
+    res["c2_cap_pdf"] = {"gsamples_s": n2 / t_cap / 1e6, "ms": t_cap}
+    res["c2_heitz_pdf"] = {"gsamples_s": n2 / t_hz / 1e6, "ms": t_hz, "t_heitz_over_t_cap": t_hz / t_cap}
+
+    # config 3: 2^28 streamed, h only
+    c3 = synth.CONFIGS[3]
+    x3 = synth.fill(c3.recipe, c3.seed, c3.n, device=dev)
+    o3 = vndf.empty_outputs(c3.n, dev, pdf=False)
+    ins3 = [x3[k] for k in synth.PLANES]
+    t_cap3 = timed(lambda: vndf.vndf_sample_cap(*ins3, *o3, stream=stream))
+    t_hz3 = timed(lambda: vndf.vndf_sample_heitz2018(*ins3, *o3, None, stream=stream))
+    rl = roofline(BYTES_PER_SAMPLE[False] * c3.n, t_cap3, "cap_c3")
+    res["c3_cap"] = {"gsamples_s": c3.n / t_cap3 / 1e6, "ms": t_cap3, "gb_s": rl["achieved"],
+                     "frac_hbm": rl["frac"]}
+    res["c3_heitz"] = {"gsamples_s": c3.n / t_hz3 / 1e6, "ms": t_hz3, "t_heitz_over_t_cap": t_hz3 / t_cap3}
+    del x3, o3, ins3
+
+    # config 5: 2^26 edge mix, h + pdf
+    c5 = synth.CONFIGS[5]
+    x5 = synth.fill(c5.recipe, c5.seed, c5.n, device=dev)
+    o5 = vndf.empty_outputs(c5.n, dev)
+    ins5 = [x5[k] for k in synth.PLANES]
+    t_cap5 = timed(lambda: vndf.vndf_sample_cap_pdf(*ins5, *o5, stream=stream))
+    t_hz5 = timed(lambda: vndf.vndf_sample_heitz2018(*ins5, *o5, stream=stream))
+    res["c5_cap_pdf"] = {"gsamples_s": c5.n / t_cap5 / 1e6, "ms": t_cap5}
+    res["c5_heitz_pdf"] = {"gsamples_s": c5.n / t_hz5 / 1e6, "ms": t_hz5, "t_heitz_over_t_cap": t_hz5 / t_cap5}
+    del x5, o5, ins5
+
+    # config 4: 2^30 fused Philox, h + pdf (17 GB written per launch)
+    c4 = synth.CONFIGS[4]
+    o4 = vndf.empty_outputs(c4.n, dev)
+    t_cap4 = timed(lambda: vndf.vndf_sample_cap_philox(c4.seed, 0, c4.n, *o4, stream=stream))
+    t_hz4 = timed(lambda: vndf.vndf_sample_heitz2018_philox(c4.seed, 0, c4.n, *o4, stream=stream))
+    res["c4_cap_philox"] = {"gsamples_s": c4.n / t_cap4 / 1e6, "ms": t_cap4,
+                            "write_gb_s": 16 * c4.n / t_cap4 / 1e6}
+    res["c4_heitz_philox"] = {"gsamples_s": c4.n / t_hz4 / 1e6, "ms": t_hz4,
+                              "t_heitz_over_t_cap": t_hz4 / t_cap4}
+    del o4
+    torch.cuda.empty_cache()
+    for v in res.values():
+        for k in list(v):
+            if isinstance(v[k], float):
+                v[k] = round(v[k], 4)
+    return res
+
+
+def run_reference(args):
+    """The tier's reference arm: the float64 oracle, as it stands, on this box's
+    host cores; each step a bounded 2^22-sample slice of the config-2 workload."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import numpy as np
+    import oracle
+    import synth
+    oracle.build()
+    cfg = synth.CONFIGS[WORKLOAD_CID]
+    m = 1 << 22
+    x = synth.fill_numpy(cfg.recipe, cfg.seed, m)
+    planes = [x[k] for k in synth.PLANES]
+    threads = oracle.default_threads()
+    for _ in range(args.warmup):
+        oracle.batch_sample(oracle.CAP, *planes, pdf=True, threads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.batch_sample(oracle.CAP, *planes, pdf=True, threads=threads)
+    dt = time.perf_counter() - t0
+    value = m * args.steps / dt / 1e9
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (same recipe as ours)",
+        "config": {"workload": f"config 2: {cfg.label}", "samples_per_step": m,
+                   "note": "each step a bounded 2^22-sample slice of the 2^24-sample workload"},
+        "cpu_baseline": {"value": round(value, 5), "unit": UNIT, "cores": threads, "kind": "oracle",
+                         "sample": f"2^22 config-2 samples per step, {threads} threads"},
+        "e2e": {"value": round(value, 5), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+    _ = np
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

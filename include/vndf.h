@@ -1,0 +1,167 @@
+/*
+ * vndf.h -- C ABI of libvndf: batched GGX visible-normal (VNDF) sampling by
+ * the spherical-cap construction of arXiv 2306.05044, on NVIDIA B200 (sm_100a).
+ *
+ * Citations: "P:n" = line n of the paper's LaTeX source.
+ *
+ * The operation (per sample k, all fp32, SoA planes):
+ *   inputs  wi_k = (wi_x, wi_y, wi_z)[k]  incident direction, need not be unit
+ *                                          (Listing 1 normalises after the
+ *                                          stretch)
+ *           alpha_x[k], alpha_y[k] > 0     GGX roughness, M^-1 = diag(ax, ay, 1)
+ *
+ *           u1[k], u2[k] in [0, 1)         two uniforms
+ *   outputs h_k = (h_x, h_y, h_z)[k]       unit visible normal, distributed as
+ *                                          the VNDF D_vis(h, wi) of Eq. 1
+ *           pdf[k]                         D_vis(h_k, wi_k), Eq. 1
+ *                                          = G1(wi) max(0, wi.h) D(h) / wi.z
+ *                                          (Eq. 12, 16-17)
+ *   method  Listing 1 around Listing 3 (spherical cap:
+ *           phi = 2 pi u1, z uniform on (-wi_std.z, 1] from u2, h_std = c +
+ *           wi_std, normalised after the unstretch), or around
+ *           Listing 2 (Heitz 2018 cross section) for the baseline.
+ *   below-horizon incidence (wi.z < 0; -0.0 counts as upper): sampled on the
+ *           flipped hemisphere, h = s * sample(s * wi), s = -1, and
+ *           pdf(h | wi) = pdf(s h | s wi)   (reading R4).
+ *
+ * Accuracy contract (BASELINE.json north_star): against the float64 oracle on
+ * identical inputs, max |dh| <= 2e-5 per component and |dpdf|/pdf <= 1e-4 for
+ * the spherical-cap entry points, on every sample in the domain alpha in
+ * [1e-3, 1], |wi| in [0.5, 2], u in [0, 1).  Ill-conditioned samples are
+ * detected in-kernel and recomputed in float64.  The
+ * Heitz baseline is the literal fp32 Listing 2 and carries no such guarantee.
+ *
+ * Ownership and behaviour (all entry points):
+ *   - Every pointer argument of the sampling calls is a CUDA DEVICE pointer
+ *     (except the *_host call), owned by the caller; the library never frees
+ *     or retains it.  Buffers hold n fp32 elements (words: 4n uint32).
+ *   - Any 4-byte aligned pointer is accepted.  When all planes of a call are
+ *     32-byte aligned a 256-bit vector path runs, 16-byte aligned a 128-bit
+ *     path, otherwise a scalar path; results are identical.
+ *   - Calls only ENQUEUE work on `stream` (NULL = legacy default stream) and
+ *     return; outputs are valid once the caller synchronises the stream.
+ *     The *_host call is the exception: it is blocking.
+ *   - Thread-safe; the only global state is a per-device cache of device
+ *     attributes and launch configurations.
+ *   - Outputs are a pure function of the inputs (of seed and global index for
+ *     the Philox calls): independent of grid, stream, vector path or chunking.
+ *
+ * Errors:
+ *   n == 0                         -> VNDF_OK, nothing enqueued
+ *   n < 0, required pointer NULL,  -> VNDF_ERR_INVALID_ARGUMENT, nothing
+ *   an output aliasing an input      enqueued
+ *   or another output, pointer not
+ *   4-byte aligned
+ *   CUDA launch / runtime failure  -> VNDF_ERR_CUDA; vndf_last_cuda_error()
+ *                                     returns the cudaError_t (thread-local)
+ *   Outside the per-sample domain the result is unspecified but never traps.
+ */
+#ifndef VNDF_H_
+#define VNDF_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Same type as cudaStream_t / CUstream; NULL is the legacy default stream. */
+typedef struct CUstream_st *vndf_stream_t;
+
+typedef enum {
+    VNDF_OK = 0,
+    VNDF_ERR_INVALID_ARGUMENT = 1,
+    VNDF_ERR_CUDA = 2,
+    VNDF_ERR_NOT_IMPLEMENTED = 3
+} vndf_status;
+
+/* Spherical-cap sampling, h only (BASELINE config 3: 28 B in, 12 B out per
+ * sample).  Listing 1 + Listing 3. */
+vndf_status vndf_sample_cap(const float *wi_x, const float *wi_y, const float *wi_z,
+                            const float *alpha_x, const float *alpha_y,
+                            const float *u1, const float *u2,
+                            float *h_x, float *h_y, float *h_z,
+                            int64_t n, vndf_stream_t stream);
+
+/* Spherical-cap sampling plus the VNDF pdf of each sample, Eq. 1
+ * (BASELINE configs 1, 2, 5: 28 B in, 16 B out per sample). */
+vndf_status vndf_sample_cap_pdf(const float *wi_x, const float *wi_y, const float *wi_z,
+                                const float *alpha_x, const float *alpha_y,
+                                const float *u1, const float *u2,
+                                float *h_x, float *h_y, float *h_z, float *pdf,
+                                int64_t n, vndf_stream_t stream);
+
+/* Same-harness baseline: Listing 1 around Heitz's cross-section sampler,
+ * Listing 2, literal fp32.  pdf may be NULL (h only). */
+vndf_status vndf_sample_heitz2018(const float *wi_x, const float *wi_y, const float *wi_z,
+                                  const float *alpha_x, const float *alpha_y,
+                                  const float *u1, const float *u2,
+                                  float *h_x, float *h_y, float *h_z, float *pdf,
+                                  int64_t n, vndf_stream_t stream);
+
+/* Fused in-kernel Philox4x32-10 (BASELINE config 4).  Sample k of the call
+ * has global index i = first_index + k; its inputs are generated from
+ * X = Philox(counter (i_lo, i_hi, 0, 0), key (seed_lo, seed_hi)) and
+ * Y = Philox(counter (i_lo, i_hi, 1, 0), same key), u(w) = (w >> 8) 2^-24:
+ *   wi uniform on the upper hemisphere: z = 1 - u(X0),
+ *      r = sqrt(u(X0) (2 - u(X0))), phi = 2 pi u(X1);
+ *   alpha_x = 0.01 * 100^u(X2), alpha_y = 0.01 * 100^u(X3);
+ *   u1 = u(Y0), u2 = u(Y1).
+ * Outputs h and pdf (16 B per sample); pdf may be NULL. */
+vndf_status vndf_sample_cap_philox(uint64_t seed, uint64_t first_index, int64_t n,
+                                   float *h_x, float *h_y, float *h_z, float *pdf,
+                                   vndf_stream_t stream);
+
+/* Heitz-2018 baseline on the same Philox inputs. pdf may be NULL. */
+vndf_status vndf_sample_heitz2018_philox(uint64_t seed, uint64_t first_index, int64_t n,
+                                         float *h_x, float *h_y, float *h_z, float *pdf,
+                                         vndf_stream_t stream);
+
+/* Raw Philox4x32-10 words of block `block` for global indices
+ * first_index .. first_index + n - 1: words[4k .. 4k+3] (test / audit). */
+vndf_status vndf_philox4x32_10(uint64_t seed, uint64_t first_index, int64_t n,
+                               uint32_t block, uint32_t *words, vndf_stream_t stream);
+
+/* End-to-end form of vndf_sample_cap_pdf on HOST buffers (pinned memory
+ * recommended; pageable works but is slower).  Streams the batch through the
+ * GPU in chunks, overlapping host->device copies, the kernel and
+ * device->host copies on two streams; device staging is stream-ordered
+ * (cudaMallocAsync) and released before return.  BLOCKING: returns when the
+ * outputs are in host memory.  Work is ordered after prior work on `stream`. */
+vndf_status vndf_sample_cap_pdf_host(const float *wi_x, const float *wi_y, const float *wi_z,
+                                     const float *alpha_x, const float *alpha_y,
+                                     const float *u1, const float *u2,
+                                     float *h_x, float *h_y, float *h_z, float *pdf,
+                                     int64_t n, vndf_stream_t stream);
+
+/* Diagnostic: number of samples the spherical-cap kernels would route to the
+ * float64 recomputation for these inputs; ADDS the count to *count (device
+ * pointer to one uint64).  Does not write samples. */
+vndf_status vndf_count_fixups(const float *wi_x, const float *wi_y, const float *wi_z,
+                              const float *alpha_x, const float *alpha_y,
+                              const float *u1, const float *u2,
+                              int64_t n, uint64_t *count, vndf_stream_t stream);
+
+/* Diagnostic: same for the fused Philox inputs. */
+vndf_status vndf_count_fixups_philox(uint64_t seed, uint64_t first_index, int64_t n,
+                                     uint64_t *count, vndf_stream_t stream);
+
+/* Tuning knobs for the streamed kernels (process-wide; 0 = automatic).
+ * vector_width in {0, 1, 4, 8} caps the vector path; block_size 0 or 64..256 (multiple of 32);
+ * blocks_per_sm >= 0 caps the persistent grid at SMs x blocks_per_sm. */
+vndf_status vndf_set_launch_config(int vector_width, int block_size, int blocks_per_sm);
+
+/* Static description of a status code. */
+const char *vndf_status_string(vndf_status status);
+
+/* cudaError_t behind the last VNDF_ERR_CUDA returned on this thread. */
+int vndf_last_cuda_error(void);
+
+/* ABI version: 100 * major + minor. */
+int vndf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VNDF_H_ */

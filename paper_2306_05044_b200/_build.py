@@ -1,0 +1,52 @@
+"""Build libvndf.so in-tree with nvcc for sm_100a (no JIT cache, no torch ext).
+
+The shared library carries its own static CUDA runtime; it takes plain device
+pointers and a cudaStream_t, so it interoperates with torch's allocator and
+streams through the driver's primary context.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+LIB = os.path.join(HERE, "libvndf.so")
+SOURCES = [os.path.join(CSRC, "vndf.cu")]
+DEPS = SOURCES + [os.path.join(CSRC, "vndf_device.cuh"), os.path.join(ROOT, "include", "vndf.h")]
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    "-Xptxas", "-v",
+    "-shared", "-Xcompiler", "-fPIC,-O2",
+    "-cudart", "static",
+]
+
+
+def stale() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    return any(os.path.getmtime(p) > t for p in DEPS)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if force or stale():
+        cmd = [NVCC, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), *SOURCES, "-o", LIB + ".tmp"]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
+        os.replace(LIB + ".tmp", LIB)
+        log = os.path.join(HERE, "csrc", "ptxas.log")
+        with open(log, "w") as f:
+            f.write(res.stderr)
+        if verbose:
+            print(res.stderr)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force=True))

@@ -1,0 +1,645 @@
+// vndf.cu -- libvndf: sm_100a kernels and the C ABI declared in include/vndf.h.
+//
+// Citations: "P:n" = PAPER.md line n (arXiv 2306.05044).
+// describes each kernel, its roofline and its algorithmic bytes per sample.
+//
+// Kernels
+//   stream_kernel<METHOD, PDF, V>   streamed SoA sampling (cap or Heitz), V
+//                                   samples per thread per step loaded with
+//                                   one V*32-bit vector load per plane
+//                                   (V = 8: LDG.E.256 / STG.E.256 on sm_100a),
+//                                   persistent grid-stride loop, inline float64
+//                                   fix-up of flagged cap samples.
+//   philox_kernel<METHOD, PDF, V>   fused Philox4x32-10 input generation +
+//                                   sampling + pdf, stores only.
+//   philox_words_kernel             raw Philox words (bit-exactness audit).
+//   count_*_kernel                  diagnostics: how many samples get fixed up.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "vndf_device.cuh"
+#include "../../include/vndf.h"
+
+using namespace vndf;
+
+namespace {
+
+enum Method { kCap = 0, kHeitz = 1 };
+
+struct StreamArgs {
+    const float* wx;
+    const float* wy;
+    const float* wz;
+    const float* ax;
+    const float* ay;
+    const float* u1;
+    const float* u2;
+    float* hx;
+    float* hy;
+    float* hz;
+    float* pdf;
+};
+
+// ---------------------------------------------------------------- memory ops
+// Streaming loads: read-only path, no L1 allocation (each byte is read once).
+template <int V>
+struct Vec {
+    float v[V];
+};
+
+template <int V>
+__device__ __forceinline__ Vec<V> ld_stream(const float* p);
+
+template <>
+__device__ __forceinline__ Vec<1> ld_stream<1>(const float* p) {
+    Vec<1> r;
+    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r.v[0]) : "l"(p));
+    return r;
+}
+template <>
+__device__ __forceinline__ Vec<4> ld_stream<4>(const float* p) {
+    Vec<4> r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3])
+                 : "l"(p));
+    return r;
+}
+template <>
+__device__ __forceinline__ Vec<8> ld_stream<8>(const float* p) {
+    Vec<8> r;
+    asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]),
+                   "=f"(r.v[4]), "=f"(r.v[5]), "=f"(r.v[6]), "=f"(r.v[7])
+                 : "l"(p));
+    return r;
+}
+
+template <int V>
+__device__ __forceinline__ void st_stream(float* p, const Vec<V>& r);
+
+template <>
+__device__ __forceinline__ void st_stream<1>(float* p, const Vec<1>& r) {
+    asm volatile("st.global.L1::no_allocate.f32 [%0], %1;" ::"l"(p), "f"(r.v[0]) : "memory");
+}
+template <>
+__device__ __forceinline__ void st_stream<4>(float* p, const Vec<4>& r) {
+    asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p),
+                 "f"(r.v[0]), "f"(r.v[1]), "f"(r.v[2]), "f"(r.v[3])
+                 : "memory");
+}
+template <>
+__device__ __forceinline__ void st_stream<8>(float* p, const Vec<8>& r) {
+    asm volatile("st.global.L1::no_allocate.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p),
+                 "f"(r.v[0]), "f"(r.v[1]), "f"(r.v[2]), "f"(r.v[3]), "f"(r.v[4]),
+                 "f"(r.v[5]), "f"(r.v[6]), "f"(r.v[7])
+                 : "memory");
+}
+
+// ------------------------------------------------------------ one sample --
+template <int METHOD, bool PDF>
+__device__ __forceinline__ Sample sample_one(float wx, float wy, float wz, float ax, float ay,
+                                             float u1, float u2) {
+    Sample o;
+    if (METHOD == kCap) {
+        const bool flag = cap_fp32<PDF>(wx, wy, wz, ax, ay, u1, u2, o);
+        if (__builtin_expect(flag, 0)) {
+            const float4 f = cap_fp64(wx, wy, wz, ax, ay, u1, u2);
+            o.x = f.x;
+            o.y = f.y;
+            o.z = f.z;
+            o.pdf = f.w;
+        }
+    } else {
+        heitz_fp32<PDF>(wx, wy, wz, ax, ay, u1, u2, o);
+    }
+    return o;
+}
+
+// ------------------------------------------------------- streamed kernel --
+// Chunk c covers samples [c V, c V + V).  Full chunks go through the vector
+// path on a persistent grid-stride loop; the n mod V tail is done by the
+// first threads of the grid with scalar accesses.
+template <int METHOD, bool PDF, int V>
+__global__ void __launch_bounds__(256) stream_kernel(StreamArgs a, int64_t n) {
+    const int64_t nchunks = n / V;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int64_t c = tid; c < nchunks; c += stride) {
+        const int64_t i = c * V;
+        const Vec<V> wx = ld_stream<V>(a.wx + i), wy = ld_stream<V>(a.wy + i),
+                     wz = ld_stream<V>(a.wz + i), ax = ld_stream<V>(a.ax + i),
+                     ay = ld_stream<V>(a.ay + i), u1 = ld_stream<V>(a.u1 + i),
+                     u2 = ld_stream<V>(a.u2 + i);
+        Vec<V> hx, hy, hz, pd;
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            const Sample o = sample_one<METHOD, PDF>(wx.v[j], wy.v[j], wz.v[j], ax.v[j],
+                                                     ay.v[j], u1.v[j], u2.v[j]);
+            hx.v[j] = o.x;
+            hy.v[j] = o.y;
+            hz.v[j] = o.z;
+            pd.v[j] = o.pdf;
+        }
+        st_stream<V>(a.hx + i, hx);
+        st_stream<V>(a.hy + i, hy);
+        st_stream<V>(a.hz + i, hz);
+        if (PDF) st_stream<V>(a.pdf + i, pd);
+    }
+    if (V > 1) {
+        const int64_t i = nchunks * V + tid;
+        if (i < n) {
+            const Sample o = sample_one<METHOD, PDF>(a.wx[i], a.wy[i], a.wz[i], a.ax[i], a.ay[i],
+                                                     a.u1[i], a.u2[i]);
+            a.hx[i] = o.x;
+            a.hy[i] = o.y;
+            a.hz[i] = o.z;
+            if (PDF) a.pdf[i] = o.pdf;
+        }
+    }
+}
+
+// ----------------------------------------------------- fused Philox kernel --
+template <int METHOD, bool PDF>
+__device__ __forceinline__ Sample philox_one(uint64_t seed, uint64_t gi) {
+    uint4 X, Y;
+    philox_xy(seed, gi, X, Y);
+    const Inputs in = c4_inputs_fp32(X, Y);
+    Sample o;
+    if (METHOD == kCap) {
+        const bool flag = cap_fp32<PDF>(in.wx, in.wy, in.wz, in.ax, in.ay, in.u1, in.u2, o);
+        if (__builtin_expect(flag, 0)) {
+            const float4 f = cap_philox_fp64(seed, gi);
+            o.x = f.x;
+            o.y = f.y;
+            o.z = f.z;
+            o.pdf = f.w;
+        }
+    } else {
+        heitz_fp32<PDF>(in.wx, in.wy, in.wz, in.ax, in.ay, in.u1, in.u2, o);
+    }
+    return o;
+}
+
+template <int METHOD, bool PDF, int V>
+__global__ void __launch_bounds__(256) philox_kernel(uint64_t seed, uint64_t first, int64_t n,
+                                                     float* __restrict__ hxp, float* __restrict__ hyp,
+                                                     float* __restrict__ hzp, float* __restrict__ pdfp) {
+    const int64_t nchunks = n / V;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int64_t c = tid; c < nchunks; c += stride) {
+        const int64_t i = c * V;
+        Vec<V> hx, hy, hz, pd;
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            const Sample o = philox_one<METHOD, PDF>(seed, first + (uint64_t)(i + j));
+            hx.v[j] = o.x;
+            hy.v[j] = o.y;
+            hz.v[j] = o.z;
+            pd.v[j] = o.pdf;
+        }
+        st_stream<V>(hxp + i, hx);
+        st_stream<V>(hyp + i, hy);
+        st_stream<V>(hzp + i, hz);
+        if (PDF) st_stream<V>(pdfp + i, pd);
+    }
+    if (V > 1) {
+        const int64_t i = nchunks * V + tid;
+        if (i < n) {
+            const Sample o = philox_one<METHOD, PDF>(seed, first + (uint64_t)i);
+            hxp[i] = o.x;
+            hyp[i] = o.y;
+            hzp[i] = o.z;
+            if (PDF) pdfp[i] = o.pdf;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) philox_words_kernel(uint64_t seed, uint64_t first, int64_t n,
+                                                           uint32_t block, uint4* __restrict__ out) {
+    const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+        const uint64_t i = first + (uint64_t)k;
+        out[k] = philox4x32_10(make_uint4((uint32_t)i, (uint32_t)(i >> 32), block, 0u), key);
+    }
+}
+
+// ------------------------------------------------------------ diagnostics --
+__device__ __forceinline__ void warp_count(bool flag, unsigned long long* count) {
+    const unsigned m = __ballot_sync(0xffffffffu, flag);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(count, (unsigned long long)__popc(m));
+}
+
+__global__ void __launch_bounds__(256) count_stream_kernel(StreamArgs a, int64_t n,
+                                                           unsigned long long* count) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t start = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t rounds = (n + stride - 1) / stride;  // uniform trip count for the ballot
+    for (int64_t r = 0; r < rounds; ++r) {
+        const int64_t i = start + r * stride;
+        bool flag = false;
+        if (i < n) {
+            Sample o;
+            flag = cap_fp32<true>(a.wx[i], a.wy[i], a.wz[i], a.ax[i], a.ay[i], a.u1[i], a.u2[i], o);
+        }
+        warp_count(flag, count);
+    }
+}
+
+__global__ void __launch_bounds__(256) count_philox_kernel(uint64_t seed, uint64_t first, int64_t n,
+                                                           unsigned long long* count) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t start = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t rounds = (n + stride - 1) / stride;
+    for (int64_t r = 0; r < rounds; ++r) {
+        const int64_t i = start + r * stride;
+        bool flag = false;
+        if (i < n) {
+            uint4 X, Y;
+            philox_xy(seed, first + (uint64_t)i, X, Y);
+            const Inputs in = c4_inputs_fp32(X, Y);
+            Sample o;
+            flag = cap_fp32<true>(in.wx, in.wy, in.wz, in.ax, in.ay, in.u1, in.u2, o);
+        }
+        warp_count(flag, count);
+    }
+}
+
+// =============================================================== host side ==
+thread_local int g_last_cuda_error = 0;
+
+struct LaunchPrefs {
+    int vector_width = 0;   // 0 = widest the alignment allows
+    int block_size = 0;     // 0 = 256
+    int blocks_per_sm = 0;  // 0 = occupancy
+};
+std::mutex g_mu;
+LaunchPrefs g_prefs;
+std::map<std::tuple<int, const void*, int>, int> g_occ;  // (device, kernel, block) -> blocks/SM
+std::map<int, int> g_sms;
+
+vndf_status cuda_fail(cudaError_t e) {
+    g_last_cuda_error = (int)e;
+    return VNDF_ERR_CUDA;
+}
+
+LaunchPrefs prefs() {
+    std::lock_guard<std::mutex> lk(g_mu);
+    return g_prefs;
+}
+
+// Persistent grid: min(work, SMs x resident blocks per SM).
+cudaError_t grid_for(const void* kernel, int block, int64_t work_items, int* grid) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    int sms = 0, occ = 0;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        auto it = g_sms.find(dev);
+        if (it != g_sms.end()) sms = it->second;
+        auto jt = g_occ.find(std::make_tuple(dev, kernel, block));
+        if (jt != g_occ.end()) occ = jt->second;
+    }
+    if (sms == 0) {
+        e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e != cudaSuccess) return e;
+        std::lock_guard<std::mutex> lk(g_mu);
+        g_sms[dev] = sms;
+    }
+    if (occ == 0) {
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, block, 0);
+        if (e != cudaSuccess) return e;
+        if (occ < 1) occ = 1;
+        std::lock_guard<std::mutex> lk(g_mu);
+        g_occ[std::make_tuple(dev, kernel, block)] = occ;
+    }
+    const LaunchPrefs p = prefs();
+    if (p.blocks_per_sm > 0) occ = std::min(occ, p.blocks_per_sm);
+    const int64_t need = std::max<int64_t>(1, (work_items + block - 1) / block);
+    *grid = (int)std::min<int64_t>(need, (int64_t)sms * occ);
+    return cudaSuccess;
+}
+
+int block_size() {
+    const int b = prefs().block_size;
+    return b > 0 ? b : 256;
+}
+
+bool aligned(const void* p, uintptr_t a) { return ((uintptr_t)p % a) == 0; }
+
+bool overlaps(const void* a, const void* b, int64_t bytes) {
+    const uintptr_t x = (uintptr_t)a, y = (uintptr_t)b;
+    return x < y + (uintptr_t)bytes && y < x + (uintptr_t)bytes;
+}
+
+// Validate a streamed call: all inputs non-NULL, required outputs non-NULL,
+// everything 4-byte aligned, no output overlapping an input or an output.
+vndf_status validate_stream(const StreamArgs& a, bool need_pdf, int64_t n) {
+    if (n < 0) return VNDF_ERR_INVALID_ARGUMENT;
+    const void* in[7] = {a.wx, a.wy, a.wz, a.ax, a.ay, a.u1, a.u2};
+    const void* out[4] = {a.hx, a.hy, a.hz, a.pdf};
+    const int nout = a.pdf ? 4 : 3;
+    for (auto p : in)
+        if (!p || !aligned(p, 4)) return VNDF_ERR_INVALID_ARGUMENT;
+    for (int k = 0; k < 3; ++k)
+        if (!out[k] || !aligned(out[k], 4)) return VNDF_ERR_INVALID_ARGUMENT;
+    if (need_pdf && !a.pdf) return VNDF_ERR_INVALID_ARGUMENT;
+    if (a.pdf && !aligned(a.pdf, 4)) return VNDF_ERR_INVALID_ARGUMENT;
+    const int64_t bytes = n * (int64_t)sizeof(float);
+    if (n > 0) {
+        for (int k = 0; k < nout; ++k) {
+            for (auto p : in)
+                if (overlaps(out[k], p, bytes)) return VNDF_ERR_INVALID_ARGUMENT;
+            for (int l = k + 1; l < nout; ++l)
+                if (overlaps(out[k], out[l], bytes)) return VNDF_ERR_INVALID_ARGUMENT;
+        }
+    }
+    return VNDF_OK;
+}
+
+int widest_vector(const StreamArgs& a) {
+    const void* all[11] = {a.wx, a.wy, a.wz, a.ax, a.ay, a.u1, a.u2, a.hx, a.hy, a.hz, a.pdf};
+    int v = 8;
+    for (auto p : all) {
+        if (!p) continue;
+        if (!aligned(p, 32)) v = std::min(v, 4);
+        if (!aligned(p, 16)) v = 1;
+    }
+    const int cap = prefs().vector_width;
+    if (cap == 1) v = 1;
+    if (cap == 4) v = std::min(v, 4);
+    return v;
+}
+
+template <int METHOD, bool PDF, int V>
+vndf_status launch_stream_v(const StreamArgs& a, int64_t n, cudaStream_t s) {
+    const void* k = (const void*)stream_kernel<METHOD, PDF, V>;
+    const int block = block_size();
+    int grid = 0;
+    cudaError_t e = grid_for(k, block, std::max<int64_t>(n / V, 1), &grid);
+    if (e != cudaSuccess) return cuda_fail(e);
+    stream_kernel<METHOD, PDF, V><<<grid, block, 0, s>>>(a, n);
+    e = cudaGetLastError();
+    return e == cudaSuccess ? VNDF_OK : cuda_fail(e);
+}
+
+template <int METHOD, bool PDF>
+vndf_status launch_stream(const StreamArgs& a, int64_t n, cudaStream_t s) {
+    switch (widest_vector(a)) {
+        case 8: return launch_stream_v<METHOD, PDF, 8>(a, n, s);
+        case 4: return launch_stream_v<METHOD, PDF, 4>(a, n, s);
+        default: return launch_stream_v<METHOD, PDF, 1>(a, n, s);
+    }
+}
+
+StreamArgs make_args(const float* wx, const float* wy, const float* wz, const float* ax,
+                     const float* ay, const float* u1, const float* u2, float* hx, float* hy,
+                     float* hz, float* pdf) {
+    StreamArgs a;
+    a.wx = wx; a.wy = wy; a.wz = wz; a.ax = ax; a.ay = ay; a.u1 = u1; a.u2 = u2;
+    a.hx = hx; a.hy = hy; a.hz = hz; a.pdf = pdf;
+    return a;
+}
+
+vndf_status validate_philox_out(int64_t n, float* hx, float* hy, float* hz, float* pdf) {
+    if (n < 0 || !hx || !hy || !hz) return VNDF_ERR_INVALID_ARGUMENT;
+    float* out[4] = {hx, hy, hz, pdf};
+    const int nout = pdf ? 4 : 3;
+    for (int k = 0; k < nout; ++k)
+        if (!aligned(out[k], 4)) return VNDF_ERR_INVALID_ARGUMENT;
+    const int64_t bytes = n * (int64_t)sizeof(float);
+    if (n > 0)
+        for (int k = 0; k < nout; ++k)
+            for (int l = k + 1; l < nout; ++l)
+                if (overlaps(out[k], out[l], bytes)) return VNDF_ERR_INVALID_ARGUMENT;
+    return VNDF_OK;
+}
+
+template <int METHOD, bool PDF, int V>
+vndf_status launch_philox_v(uint64_t seed, uint64_t first, int64_t n, float* hx, float* hy, float* hz,
+                            float* pdf, cudaStream_t s) {
+    const void* k = (const void*)philox_kernel<METHOD, PDF, V>;
+    const int block = block_size();
+    int grid = 0;
+    cudaError_t e = grid_for(k, block, std::max<int64_t>(n / V, 1), &grid);
+    if (e != cudaSuccess) return cuda_fail(e);
+    philox_kernel<METHOD, PDF, V><<<grid, block, 0, s>>>(seed, first, n, hx, hy, hz, pdf);
+    e = cudaGetLastError();
+    return e == cudaSuccess ? VNDF_OK : cuda_fail(e);
+}
+
+template <int METHOD>
+vndf_status launch_philox(uint64_t seed, uint64_t first, int64_t n, float* hx, float* hy, float* hz,
+                          float* pdf, cudaStream_t s) {
+    vndf_status st = validate_philox_out(n, hx, hy, hz, pdf);
+    if (st != VNDF_OK || n == 0) return st;
+    bool v4 = aligned(hx, 16) && aligned(hy, 16) && aligned(hz, 16) && (!pdf || aligned(pdf, 16));
+    if (prefs().vector_width == 1) v4 = false;
+    if (pdf) {
+        return v4 ? launch_philox_v<METHOD, true, 4>(seed, first, n, hx, hy, hz, pdf, s)
+                  : launch_philox_v<METHOD, true, 1>(seed, first, n, hx, hy, hz, pdf, s);
+    }
+    return v4 ? launch_philox_v<METHOD, false, 4>(seed, first, n, hx, hy, hz, pdf, s)
+              : launch_philox_v<METHOD, false, 1>(seed, first, n, hx, hy, hz, pdf, s);
+}
+
+}  // namespace
+
+// ================================================================== C ABI ==
+extern "C" {
+
+vndf_status vndf_sample_cap(const float* wi_x, const float* wi_y, const float* wi_z,
+                            const float* alpha_x, const float* alpha_y, const float* u1,
+                            const float* u2, float* h_x, float* h_y, float* h_z, int64_t n,
+                            vndf_stream_t stream) {
+    const StreamArgs a = make_args(wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, h_x, h_y, h_z, nullptr);
+    vndf_status st = validate_stream(a, false, n);
+    if (st != VNDF_OK || n == 0) return st;
+    return launch_stream<kCap, false>(a, n, (cudaStream_t)stream);
+}
+
+vndf_status vndf_sample_cap_pdf(const float* wi_x, const float* wi_y, const float* wi_z,
+                                const float* alpha_x, const float* alpha_y, const float* u1,
+                                const float* u2, float* h_x, float* h_y, float* h_z, float* pdf,
+                                int64_t n, vndf_stream_t stream) {
+    const StreamArgs a = make_args(wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, h_x, h_y, h_z, pdf);
+    vndf_status st = validate_stream(a, true, n);
+    if (st != VNDF_OK || n == 0) return st;
+    return launch_stream<kCap, true>(a, n, (cudaStream_t)stream);
+}
+
+vndf_status vndf_sample_heitz2018(const float* wi_x, const float* wi_y, const float* wi_z,
+                                  const float* alpha_x, const float* alpha_y, const float* u1,
+                                  const float* u2, float* h_x, float* h_y, float* h_z, float* pdf,
+                                  int64_t n, vndf_stream_t stream) {
+    const StreamArgs a = make_args(wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, h_x, h_y, h_z, pdf);
+    vndf_status st = validate_stream(a, false, n);
+    if (st != VNDF_OK || n == 0) return st;
+    return pdf ? launch_stream<kHeitz, true>(a, n, (cudaStream_t)stream)
+               : launch_stream<kHeitz, false>(a, n, (cudaStream_t)stream);
+}
+
+vndf_status vndf_sample_cap_philox(uint64_t seed, uint64_t first_index, int64_t n, float* h_x,
+                                   float* h_y, float* h_z, float* pdf, vndf_stream_t stream) {
+    return launch_philox<kCap>(seed, first_index, n, h_x, h_y, h_z, pdf, (cudaStream_t)stream);
+}
+
+vndf_status vndf_sample_heitz2018_philox(uint64_t seed, uint64_t first_index, int64_t n, float* h_x,
+                                         float* h_y, float* h_z, float* pdf, vndf_stream_t stream) {
+    return launch_philox<kHeitz>(seed, first_index, n, h_x, h_y, h_z, pdf, (cudaStream_t)stream);
+}
+
+vndf_status vndf_philox4x32_10(uint64_t seed, uint64_t first_index, int64_t n, uint32_t block,
+                               uint32_t* words, vndf_stream_t stream) {
+    if (n < 0 || !words || !aligned(words, 16)) return VNDF_ERR_INVALID_ARGUMENT;
+    if (n == 0) return VNDF_OK;
+    int grid = 0;
+    cudaError_t e = grid_for((const void*)philox_words_kernel, 256, n, &grid);
+    if (e != cudaSuccess) return cuda_fail(e);
+    philox_words_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(seed, first_index, n, block,
+                                                                 (uint4*)words);
+    e = cudaGetLastError();
+    return e == cudaSuccess ? VNDF_OK : cuda_fail(e);
+}
+
+vndf_status vndf_count_fixups(const float* wi_x, const float* wi_y, const float* wi_z,
+                              const float* alpha_x, const float* alpha_y, const float* u1,
+                              const float* u2, int64_t n, uint64_t* count, vndf_stream_t stream) {
+    if (n < 0 || !count || !aligned(count, 8)) return VNDF_ERR_INVALID_ARGUMENT;
+    const void* in[7] = {wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2};
+    for (auto p : in)
+        if (!p || !aligned(p, 4)) return VNDF_ERR_INVALID_ARGUMENT;
+    if (n == 0) return VNDF_OK;
+    const StreamArgs a = make_args(wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, nullptr, nullptr,
+                                   nullptr, nullptr);
+    int grid = 0;
+    cudaError_t e = grid_for((const void*)count_stream_kernel, 256, n, &grid);
+    if (e != cudaSuccess) return cuda_fail(e);
+    count_stream_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(a, n, (unsigned long long*)count);
+    e = cudaGetLastError();
+    return e == cudaSuccess ? VNDF_OK : cuda_fail(e);
+}
+
+vndf_status vndf_count_fixups_philox(uint64_t seed, uint64_t first_index, int64_t n, uint64_t* count,
+                                     vndf_stream_t stream) {
+    if (n < 0 || !count || !aligned(count, 8)) return VNDF_ERR_INVALID_ARGUMENT;
+    if (n == 0) return VNDF_OK;
+    int grid = 0;
+    cudaError_t e = grid_for((const void*)count_philox_kernel, 256, n, &grid);
+    if (e != cudaSuccess) return cuda_fail(e);
+    count_philox_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(seed, first_index, n,
+                                                                 (unsigned long long*)count);
+    e = cudaGetLastError();
+    return e == cudaSuccess ? VNDF_OK : cuda_fail(e);
+}
+
+vndf_status vndf_sample_cap_pdf_host(const float* wi_x, const float* wi_y, const float* wi_z,
+                                     const float* alpha_x, const float* alpha_y, const float* u1,
+                                     const float* u2, float* h_x, float* h_y, float* h_z, float* pdf,
+                                     int64_t n, vndf_stream_t stream) {
+    const StreamArgs host = make_args(wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, h_x, h_y, h_z, pdf);
+    vndf_status st = validate_stream(host, true, n);
+    if (st != VNDF_OK || n == 0) return st;
+    cudaStream_t user = (cudaStream_t)stream;
+    const int64_t chunk = std::min<int64_t>(n, (int64_t)1 << 22);
+    const int nsets = 2;
+    const size_t set_floats = (size_t)chunk * 11;
+    float* dbuf = nullptr;
+    cudaStream_t ss[2] = {nullptr, nullptr};
+    cudaEvent_t ready = nullptr, done[2] = {nullptr, nullptr};
+    cudaError_t e = cudaSuccess;
+    vndf_status result = VNDF_OK;
+#define VNDF_TRY(x)                 \
+    do {                            \
+        e = (x);                    \
+        if (e != cudaSuccess) goto fail; \
+    } while (0)
+    VNDF_TRY(cudaStreamCreateWithFlags(&ss[0], cudaStreamNonBlocking));
+    VNDF_TRY(cudaStreamCreateWithFlags(&ss[1], cudaStreamNonBlocking));
+    VNDF_TRY(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    VNDF_TRY(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming));
+    VNDF_TRY(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming));
+    VNDF_TRY(cudaMallocAsync((void**)&dbuf, set_floats * nsets * sizeof(float), user));
+    VNDF_TRY(cudaEventRecord(ready, user));
+    VNDF_TRY(cudaStreamWaitEvent(ss[0], ready, 0));
+    VNDF_TRY(cudaStreamWaitEvent(ss[1], ready, 0));
+    for (int64_t off = 0, c = 0; off < n; off += chunk, ++c) {
+        const int64_t m = std::min<int64_t>(chunk, n - off);
+        cudaStream_t s = ss[c % 2];
+        float* base = dbuf + (size_t)(c % 2) * set_floats;
+        float* d[11];
+        for (int k = 0; k < 11; ++k) d[k] = base + (size_t)k * chunk;
+        const float* hin[7] = {wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2};
+        float* hout[4] = {h_x, h_y, h_z, pdf};
+        const size_t bytes = (size_t)m * sizeof(float);
+        for (int k = 0; k < 7; ++k)
+            VNDF_TRY(cudaMemcpyAsync(d[k], hin[k] + off, bytes, cudaMemcpyHostToDevice, s));
+        const StreamArgs da = make_args(d[0], d[1], d[2], d[3], d[4], d[5], d[6], d[7], d[8], d[9], d[10]);
+        result = launch_stream<kCap, true>(da, m, s);
+        if (result != VNDF_OK) goto fail_status;
+        for (int k = 0; k < 4; ++k)
+            VNDF_TRY(cudaMemcpyAsync(hout[k] + off, d[7 + k], bytes, cudaMemcpyDeviceToHost, s));
+    }
+    VNDF_TRY(cudaEventRecord(done[0], ss[0]));
+    VNDF_TRY(cudaEventRecord(done[1], ss[1]));
+    VNDF_TRY(cudaStreamWaitEvent(user, done[0], 0));
+    VNDF_TRY(cudaStreamWaitEvent(user, done[1], 0));
+    VNDF_TRY(cudaFreeAsync(dbuf, user));
+    dbuf = nullptr;
+    VNDF_TRY(cudaStreamSynchronize(user));
+    for (auto x : ss) cudaStreamDestroy(x);
+    cudaEventDestroy(ready);
+    for (auto x : done) cudaEventDestroy(x);
+    return VNDF_OK;
+#undef VNDF_TRY
+fail:
+    result = cuda_fail(e);
+fail_status:
+    if (ss[0]) cudaStreamSynchronize(ss[0]);
+    if (ss[1]) cudaStreamSynchronize(ss[1]);
+    if (dbuf) cudaFreeAsync(dbuf, user);
+    cudaStreamSynchronize(user);
+    for (auto x : ss)
+        if (x) cudaStreamDestroy(x);
+    if (ready) cudaEventDestroy(ready);
+    for (auto x : done)
+        if (x) cudaEventDestroy(x);
+    return result;
+}
+
+vndf_status vndf_set_launch_config(int vector_width, int block_size, int blocks_per_sm) {
+    if (!(vector_width == 0 || vector_width == 1 || vector_width == 4 || vector_width == 8))
+        return VNDF_ERR_INVALID_ARGUMENT;
+    if (!(block_size == 0 || (block_size >= 64 && block_size <= 256 && block_size % 32 == 0)))
+        return VNDF_ERR_INVALID_ARGUMENT;
+    if (blocks_per_sm < 0) return VNDF_ERR_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_prefs.vector_width = vector_width;
+    g_prefs.block_size = block_size;
+    g_prefs.blocks_per_sm = blocks_per_sm;
+    return VNDF_OK;
+}
+
+const char* vndf_status_string(vndf_status status) {
+    switch (status) {
+        case VNDF_OK: return "VNDF_OK";
+        case VNDF_ERR_INVALID_ARGUMENT: return "VNDF_ERR_INVALID_ARGUMENT";
+        case VNDF_ERR_CUDA: return "VNDF_ERR_CUDA";
+        case VNDF_ERR_NOT_IMPLEMENTED: return "VNDF_ERR_NOT_IMPLEMENTED";
+    }
+    return "VNDF_ERR_UNKNOWN";
+}
+
+int vndf_last_cuda_error(void) { return g_last_cuda_error; }
+
+int vndf_version(void) { return 100; }
+
+}  // extern "C"

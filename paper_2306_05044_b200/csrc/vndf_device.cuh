@@ -1,0 +1,265 @@
+// vndf_device.cuh -- per-sample device arithmetic of libvndf (sm_100a).
+//
+// Citations: "P:n" = PAPER.md line n (arXiv 2306.05044 LaTeX source).
+// This file is the product path.  It shares nothing with oracle/ (the float64
+// CPU oracle used only by the tests).
+//
+// Layout of the arithmetic:
+//   * the spherical-cap sampler is Listing 1 + Listing 3 rewritten in an
+//     algebraically identical, cancellation-free fp32 form;
+//   * each sample carries a conditioning flag; flagged samples are recomputed
+//     in float64 (cap_fp64) so the 2e-5 / 1e-4 contract holds on every sample;
+//   * the Heitz-2018 baseline is Listing 2 taken literally, with the same
+//     primitive functions (same harness) and no fix-up.
+#pragma once
+
+#include <cstdint>
+
+namespace vndf {
+
+constexpr float kPiF = 3.14159265358979323846f;
+constexpr double kPiD = 3.14159265358979323846;
+
+// ---------------------------------------------------------------------------
+// Conditioning flag thresholds ("error budget").
+// The fp32 half vector hs = c + ws carries an absolute error e ~ 2e-7 (fp32
+// rounding of O(1) terms plus sincospif's ulp).  The unstretch divides it by
+// |m| = |diag(ax, ay, 1) hs| after multiplying it by at most max(ax, ay):
+// |dh| ~ e max(a) / |m|.  The pdf |m|^3 / (pi ax ay a |hs|^2) carries
+// ~3 e max(a)/|m| + 2 e/|hs| relative error.  Samples outside
+//     |m|^2 >= kFlagM * max(a)^2   and   |hs|^2 >= kFlagHs
+// are recomputed in float64.
+// ---------------------------------------------------------------------------
+constexpr float kFlagM = 4.0e-3f;   // |m| < 0.063 max(a)  -> |dh| ~> 3e-6
+constexpr float kFlagHs = 1.0e-3f;  // |hs| < 0.032         -> pdf rel ~> 1.2e-5
+
+// ---------------------------------------------------------------------------
+// Explicit single-instruction SFU approximations (MUFU.RSQ / SQRT / RCP).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float rsqrt_approx(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// sin(2 pi u), cos(2 pi u) for u in [0, 1): phi = 2 pi u1 (Listing 3,
+// Listing 2).  sincospif is accurate to ~1 ulp on the whole range.
+__device__ __forceinline__ void sincos_2pi(float u, float* s, float* c) {
+    sincospif(2.0f * u, s, c);
+}
+
+struct Sample {
+    float x, y, z, pdf;
+};
+
+// ---------------------------------------------------------------------------
+// Spherical-cap VNDF sample, fp32 (Listing 1 P:415-427 + Listing 3
+// P:523-539), plus the Eq. 1 pdf.  Returns the conditioning flag.
+//
+// Cancellation-free algebra (identical in exact arithmetic to Listing 3):
+//   a = 1 + ws.z,  q = 1 - u2,  z = q a - ws.z
+//   hs.z = z + ws.z = q a                                  (no cancel)
+//   1 - z = u2 a,  1 + z = q a + (1 - ws.z) = q a + rs^2 / a,
+//   rs^2 = ws.x^2 + ws.y^2 = (1 - ws.z)(1 + ws.z)
+//   sin^2(theta) = (1 - z)(1 + z) = u2 (q a^2 + rs^2)
+// pdf: with |c| = |ws| = 1, hs.ws = |hs|^2 / 2, so Eq. 1 with Eq. 2-4
+//   D_vis = 2 (hs.ws) |m|^3 / (pi a ax ay |hs|^4) = |m|^3 / (pi a ax ay |hs|^2),
+//   m = diag(ax, ay, 1) hs (the unnormalised output).
+// ---------------------------------------------------------------------------
+template <bool PDF>
+__device__ __forceinline__ bool cap_fp32(float wx, float wy, float wz, float ax, float ay,
+                                         float u1, float u2, Sample& o) {
+    const float s = (wz < 0.0f) ? -1.0f : 1.0f;           // reading R4 (flip)
+    // (1) warp to the hemisphere configuration: ws = M^-1 w / |M^-1 w|
+    const float tx = ax * wx, ty = ay * wy;
+    const float L2 = fmaf(tx, tx, fmaf(ty, ty, wz * wz));
+    const float sinvL = s * rsqrt_approx(L2);
+    const float wsx = tx * sinvL, wsy = ty * sinvL, wsz = wz * sinvL;
+    // (2) sample the spherical cap z in (-ws.z, 1], phi = 2 pi u1
+    const float a = 1.0f + wsz;
+    const float q = 1.0f - u2;
+    const float hz = q * a;
+    const float rs2 = fmaf(wsx, wsx, wsy * wsy);
+    const float sin2 = u2 * fmaf(hz, a, rs2);
+    const float st = sqrt_approx(sin2);
+    float sp, cp;
+    sincos_2pi(u1, &sp, &cp);
+    // half vector hs = c + ws, not normalised
+    const float hx = fmaf(st, cp, wsx), hy = fmaf(st, sp, wsy);
+    // (3) warp back with M^-T = diag(ax, ay, 1) and normalise
+    const float mx = ax * hx, my = ay * hy;
+    const float m2 = fmaf(mx, mx, fmaf(my, my, hz * hz));
+    const float invN = rsqrt_approx(m2);
+    const float t = s * invN;
+    o.x = mx * t;
+    o.y = my * t;
+    o.z = hz * t;
+    const float hs2 = fmaf(hx, hx, fmaf(hy, hy, hz * hz));
+    if (PDF) {
+        const float num = m2 * (m2 * invN);                 // |m|^3
+        const float den = (kPiF * ax * ay) * a * hs2;
+        o.pdf = num * rcp_approx(den);
+    }
+    const float amax = fmaxf(ax, ay);
+    return (m2 < kFlagM * (amax * amax)) | (hs2 < kFlagHs);
+}
+
+// ---------------------------------------------------------------------------
+// Float64 recomputation of one cap sample (the fix-up).  Same algebra as
+// cap_fp32, IEEE double throughout (sincospi, sqrt, division).
+// ---------------------------------------------------------------------------
+__device__ __noinline__ float4 cap_fp64(double wx, double wy, double wz, double ax, double ay,
+                                        double u1, double u2) {
+    const double s = (wz < 0.0) ? -1.0 : 1.0;
+    const double tx = ax * wx, ty = ay * wy;
+    const double L = sqrt(tx * tx + ty * ty + wz * wz);
+    const double wsx = s * tx / L, wsy = s * ty / L, wsz = s * wz / L;
+    const double a = 1.0 + wsz;
+    const double q = 1.0 - u2;
+    const double hz = q * a;
+    const double rs2 = wsx * wsx + wsy * wsy;
+    const double st = sqrt(u2 * (hz * a + rs2));
+    double sp, cp;
+    sincospi(2.0 * u1, &sp, &cp);
+    const double hx = st * cp + wsx, hy = st * sp + wsy;
+    const double mx = ax * hx, my = ay * hy;
+    const double m2 = mx * mx + my * my + hz * hz;
+    const double N = sqrt(m2);
+    const double hs2 = hx * hx + hy * hy + hz * hz;
+    const double pdf = m2 * N / (kPiD * ax * ay * a * hs2);
+    return make_float4((float)(s * mx / N), (float)(s * my / N), (float)(s * hz / N), (float)pdf);
+}
+
+// ---------------------------------------------------------------------------
+// Heitz-2018 baseline, fp32: Listing 1 around Listing 2 taken
+// literally, with the same SFU primitives as the cap kernel.
+// pdf: Eq. 1 for a unit std-space normal hs:
+//   D_vis = 2 max(hs.ws, 0) |m|^3 / (pi a ax ay |hs|^4).
+// ---------------------------------------------------------------------------
+template <bool PDF>
+__device__ __forceinline__ void heitz_fp32(float wx, float wy, float wz, float ax, float ay,
+                                           float u1, float u2, Sample& o) {
+    const float s = (wz < 0.0f) ? -1.0f : 1.0f;
+    const float tx = ax * wx, ty = ay * wy;
+    const float L2 = fmaf(tx, tx, fmaf(ty, ty, wz * wz));
+    const float sinvL = s * rsqrt_approx(L2);
+    const float wsx = tx * sinvL, wsy = ty * sinvL, wsz = wz * sinvL;
+    // orthonormal basis (with special case if cross product is 0)
+    const float tmp = wsx * wsx + wsy * wsy;
+    float w1x = 1.0f, w1y = 0.0f;
+    if (tmp > 0.0f) {
+        const float it = rsqrt_approx(tmp);
+        w1x = -wsy * it;
+        w1y = wsx * it;
+    }
+    // w2 = cross(ws, w1) with w1.z = 0
+    const float w2x = -wsz * w1y, w2y = wsz * w1x, w2z = wsx * w1y - wsy * w1x;
+    // parameterization of the cross section
+    float sp, cp;
+    sincos_2pi(u1, &sp, &cp);
+    const float r = sqrt_approx(u2);
+    const float t1 = r * cp;
+    float t2 = r * sp;
+    const float sh = (1.0f + wsz) * 0.5f;
+    t2 = (1.0f - sh) * sqrt_approx(1.0f - t1 * t1) + sh * t2;
+    const float ti = sqrt_approx(fmaxf(1.0f - t1 * t1 - t2 * t2, 0.0f));
+    // reprojection onto hemisphere
+    const float hx = t1 * w1x + t2 * w2x + ti * wsx;
+    const float hy = t1 * w1y + t2 * w2y + ti * wsy;
+    const float hz = t2 * w2z + ti * wsz;
+    // warp back
+    const float mx = ax * hx, my = ay * hy;
+    const float m2 = fmaf(mx, mx, fmaf(my, my, hz * hz));
+    const float invN = rsqrt_approx(m2);
+    const float t = s * invN;
+    o.x = mx * t;
+    o.y = my * t;
+    o.z = hz * t;
+    if (PDF) {
+        const float hs2 = fmaf(hx, hx, fmaf(hy, hy, hz * hz));
+        const float dotp = fmaxf(fmaf(hx, wsx, fmaf(hy, wsy, hz * wsz)), 0.0f);
+        const float num = 2.0f * dotp * m2 * (m2 * invN);
+        const float den = (kPiF * ax * ay) * (1.0f + wsz) * (hs2 * hs2);
+        o.pdf = num * rcp_approx(den);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Philox4x32-10 (Salmon et al. SC'11), counter-based: no state, any index.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t p0 = (uint64_t)0xD2511F53u * c.x;
+        const uint64_t p1 = (uint64_t)0xCD9E8D57u * c.z;
+        c = make_uint4((uint32_t)(p1 >> 32) ^ c.y ^ k.x, (uint32_t)p1,
+                       (uint32_t)(p0 >> 32) ^ c.w ^ k.y, (uint32_t)p0);
+        k.x += 0x9E3779B9u;
+        k.y += 0xBB67AE85u;
+    }
+    return c;
+}
+
+__device__ __forceinline__ float u01f(uint32_t w) {
+    return __uint2float_rn(w >> 8) * 0x1p-24f;
+}
+__device__ __forceinline__ double u01d(uint32_t w) {
+    return (double)(w >> 8) * 0x1p-24;
+}
+
+// Config-4 inputs from the two Philox blocks X, Y (vndf.h, DESIGN.md s.5).
+constexpr float kLog2_100F = 6.64385618977472436f;
+constexpr double kLog2_100D = 6.64385618977472436;
+
+struct Inputs {
+    float wx, wy, wz, ax, ay, u1, u2;
+};
+
+__device__ __forceinline__ Inputs c4_inputs_fp32(uint4 X, uint4 Y) {
+    Inputs in;
+    const float ua = u01f(X.x), ub = u01f(X.y);
+    const float r = sqrtf(ua * (2.0f - ua));   // IEEE sqrt: generation stays ~1 ulp
+    float sp, cp;
+    sincos_2pi(ub, &sp, &cp);
+    in.wx = r * cp;
+    in.wy = r * sp;
+    in.wz = 1.0f - ua;
+    // 0.01 * 100^u = 2^((u - 1) log2 100); (u - 1) is exact
+    in.ax = exp2f((u01f(X.z) - 1.0f) * kLog2_100F);
+    in.ay = exp2f((u01f(X.w) - 1.0f) * kLog2_100F);
+    in.u1 = u01f(Y.x);
+    in.u2 = u01f(Y.y);
+    return in;
+}
+
+__device__ __forceinline__ void philox_xy(uint64_t seed, uint64_t i, uint4& X, uint4& Y) {
+    const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+    X = philox4x32_10(make_uint4((uint32_t)i, (uint32_t)(i >> 32), 0u, 0u), key);
+    Y = philox4x32_10(make_uint4((uint32_t)i, (uint32_t)(i >> 32), 1u, 0u), key);
+}
+
+// Float64 fix-up for a config-4 sample: regenerate the words, build the inputs
+// in double from the exact uniforms, sample in double.
+__device__ __noinline__ float4 cap_philox_fp64(uint64_t seed, uint64_t i) {
+    uint4 X, Y;
+    philox_xy(seed, i, X, Y);
+    const double ua = u01d(X.x), ub = u01d(X.y);
+    const double r = sqrt(ua * (2.0 - ua));
+    double sp, cp;
+    sincospi(2.0 * ub, &sp, &cp);
+    const double ax = exp2((u01d(X.z) - 1.0) * kLog2_100D);
+    const double ay = exp2((u01d(X.w) - 1.0) * kLog2_100D);
+    return cap_fp64(r * cp, r * sp, 1.0 - ua, ax, ay, u01d(Y.x), u01d(Y.y));
+}
+
+}  // namespace vndf

@@ -1,0 +1,316 @@
+"""GPU parity: libvndf (through its C ABI) against the float64 oracle.
+
+Tolerances (BASELINE.json north_star), written here once:
+  spherical-cap kernels: max |dh| <= 2e-5 per component, |dpdf|/pdf <= 1e-4,
+  on EVERY compared sample; Philox words bit-exact.
+Inputs come from synth/ (seeded, counter-based; DESIGN.md s.5) and are copied
+back to the host so both sides see identical fp32 values.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+TOL_H = 2e-5
+TOL_PDF = 1e-4
+
+
+@pytest.fixture(scope="module")
+def env():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+    __graft_entry__.build()
+    import oracle
+    import paper_2306_05044_b200 as vndf
+    import synth
+    return oracle, vndf, synth, torch.device("cuda:0")
+
+
+def _host(x, keys):
+    return [x[k].cpu().numpy() for k in keys]
+
+
+def _errors(h_gpu, p_gpu, h_ref, p_ref):
+    h = np.stack(h_gpu).astype(np.float64)
+    eh = np.abs(h - h_ref).max(axis=0)
+    ep = None
+    if p_gpu is not None:
+        ep = np.abs(p_gpu.astype(np.float64) - p_ref) / p_ref
+    return eh, ep
+
+
+def _stream_run(vndf, x, keys, pdf=True, kernel="cap", stream=None):
+    n = x["wi_x"].numel()
+    dev = x["wi_x"].device
+    out = vndf.empty_outputs(n, dev, pdf=pdf)
+    ins = [x[k] for k in keys]
+    if kernel == "cap":
+        if pdf:
+            vndf.vndf_sample_cap_pdf(*ins, *out, stream=stream)
+        else:
+            vndf.vndf_sample_cap(*ins, *out, stream=stream)
+    else:
+        vndf.vndf_sample_heitz2018(*ins, *out[:3], out[3] if pdf else None, stream=stream)
+    torch.cuda.synchronize()
+    return out
+
+
+def _check_full(env, cid, n=None):
+    oracle, vndf, synth, dev = env
+    cfg = synth.CONFIGS[cid]
+    n = n or cfg.n
+    x = synth.fill(cfg.recipe, cfg.seed, n, device=dev)
+    out = _stream_run(vndf, x, synth.PLANES, pdf=cfg.pdf)
+    host = _host(x, synth.PLANES)
+    h_ref, p_ref, _ = oracle.batch_sample(oracle.CAP, *host, pdf=cfg.pdf)
+    hg = [o.cpu().numpy() for o in out[:3]]
+    pg = out[3].cpu().numpy() if cfg.pdf else None
+    eh, ep = _errors(hg, pg, h_ref, p_ref)
+    bad = np.flatnonzero(eh > TOL_H)
+    assert bad.size == 0, (cid, bad.size, float(eh.max()), [float(host[k][bad[0]]) for k in range(7)])
+    if cfg.pdf:
+        badp = np.flatnonzero(ep > TOL_PDF)
+        assert badp.size == 0, (cid, badp.size, float(ep.max()), [float(host[k][badp[0]]) for k in range(7)])
+    return float(eh.max()), (float(ep.max()) if ep is not None else None)
+
+
+def test_config1_full(env):
+    _check_full(env, 1)
+
+
+def test_config2_full(env):
+    _check_full(env, 2)
+
+
+def test_config5_full_range_subset(env):
+    # 2^22 of config 5's inputs, every sample compared (the full 2^26 is sampled below)
+    _check_full(env, 5, n=1 << 22)
+
+
+def test_config3_range_subset_h_only(env):
+    _check_full(env, 3, n=1 << 22)
+
+
+@pytest.mark.parametrize("cid", [3, 5])
+def test_full_size_sampled(env, cid):
+    """BASELINE full sizes, the launch configuration bench.py times; 2^20 sampled
+    indices (plus the first and last 4096) compared one by one."""
+    oracle, vndf, synth, dev = env
+    cfg = synth.CONFIGS[cid]
+    n = cfg.n
+    x = synth.fill(cfg.recipe, cfg.seed, n, device=dev)
+    out = _stream_run(vndf, x, synth.PLANES, pdf=cfg.pdf)
+    rng = np.random.default_rng(cid)
+    idx = np.unique(np.concatenate([rng.integers(0, n, 1 << 20), np.arange(4096), np.arange(n - 4096, n)]))
+    ti = torch.from_numpy(idx).to(dev)
+    host = [x[k][ti].cpu().numpy() for k in synth.PLANES]
+    h_ref, p_ref, _ = oracle.batch_sample(oracle.CAP, *host, pdf=cfg.pdf)
+    hg = [o[ti].cpu().numpy() for o in out[:3]]
+    pg = out[3][ti].cpu().numpy() if cfg.pdf else None
+    eh, ep = _errors(hg, pg, h_ref, p_ref)
+    assert eh.max() <= TOL_H
+    if cfg.pdf:
+        assert ep.max() <= TOL_PDF
+    # invariants on EVERY sample, evaluated on the device (properties at any size)
+    s = torch.where(x["wi_z"] < 0, -1.0, 1.0)
+    norm = torch.sqrt(out[0].double() ** 2 + out[1].double() ** 2 + out[2].double() ** 2)
+    assert float((norm - 1).abs().max()) < 2e-6
+    dot = x["wi_x"] * out[0] + x["wi_y"] * out[1] + x["wi_z"] * out[2]
+    assert float(dot.min()) >= -1e-6
+    assert float((s * out[2]).min()) >= 0.0
+    assert bool(torch.isfinite(out[0]).all() and torch.isfinite(out[2]).all())
+    if cfg.pdf:
+        assert bool(torch.isfinite(out[3]).all()) and float(out[3].min()) > 0
+
+
+def test_config4_philox_sampled(env):
+    """Config 4 at its full size (2^30, 17 GB of outputs), sampled indices."""
+    oracle, vndf, synth, dev = env
+    cfg = synth.CONFIGS[4]
+    n = cfg.n
+    out = vndf.empty_outputs(n, dev)
+    vndf.vndf_sample_cap_philox(cfg.seed, 0, n, *out)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(4)
+    idx = np.unique(np.concatenate([rng.integers(0, n, 1 << 20), np.arange(4096), np.arange(n - 4096, n)]))
+    ti = torch.from_numpy(idx).to(dev)
+    h_ref, p_ref, _ = oracle.batch_sample_philox(oracle.CAP, cfg.seed, idx)
+    hg = [o[ti].cpu().numpy() for o in out[:3]]
+    eh, ep = _errors(hg, out[3][ti].cpu().numpy(), h_ref, p_ref)
+    assert eh.max() <= TOL_H and ep.max() <= TOL_PDF, (float(eh.max()), float(ep.max()))
+    assert bool(torch.isfinite(out[3]).all()) and float(out[3].min()) > 0
+    del out
+    torch.cuda.empty_cache()
+
+
+def test_philox_full_range_small(env):
+    """Every sample of a 2^20 Philox range, across the 32-bit carry of the counter."""
+    oracle, vndf, synth, dev = env
+    for first, n in ((0, 1 << 20), ((1 << 32) - 4096, 8192 + 3)):
+        out = vndf.empty_outputs(n, dev)
+        vndf.vndf_sample_cap_philox(3, first, n, *out)
+        torch.cuda.synchronize()
+        h_ref, p_ref, _ = oracle.batch_sample_philox(oracle.CAP, 3, np.arange(first, first + n, dtype=np.uint64))
+        eh, ep = _errors([o.cpu().numpy() for o in out[:3]], out[3].cpu().numpy(), h_ref, p_ref)
+        assert eh.max() <= TOL_H and ep.max() <= TOL_PDF, (first, float(eh.max()), float(ep.max()))
+
+
+def test_philox_words_bit_exact(env):
+    oracle, vndf, synth, dev = env
+    rng = np.random.default_rng(9)
+    ranges = [(0, 1 << 20), ((1 << 32) - 1024, 2048)] + [(int(s), 1024) for s in rng.integers(0, 1 << 40, 64)]
+    for seed in (3, 0xDEADBEEFCAFEF00D):
+        for first, n in ranges:
+            for block in (0, 1):
+                w = torch.empty(4 * n, dtype=torch.int32, device=dev)
+                vndf.vndf_philox4x32_10(seed, first, n, block, w)
+                got = w.cpu().numpy().view(np.uint32).reshape(n, 4)
+                want = oracle.philox_words(seed, np.arange(first, first + n, dtype=np.uint64), block)
+                np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("n", [1, 2, 7, 8, 9, 31, 33, 4099, 65537])
+def test_ragged_sizes_and_vector_paths(env, n):
+    """Tails (n mod 8 != 0) and the three vector paths (32 B, 16 B, 4 B aligned
+    planes) give bit-identical results, all within tolerance."""
+    oracle, vndf, synth, dev = env
+    x = synth.fill(5, 4, n, device=dev)
+    results = []
+    for off in (0, 4, 1):  # 32 B, 16 B and 4 B aligned planes
+        ins = []
+        for k in synth.PLANES:
+            b = torch.zeros(n + 8, dtype=torch.float32, device=dev)
+            b[off:off + n] = x[k]
+            ins.append(b[off:off + n])
+        outs = [torch.zeros(n + 8, dtype=torch.float32, device=dev)[off:off + n] for _ in range(4)]
+        vndf.vndf_sample_cap_pdf(*ins, *outs)
+        torch.cuda.synchronize()
+        results.append([t.cpu().numpy().copy() for t in outs])
+    for r in results[1:]:
+        for a, b in zip(results[0], r):
+            np.testing.assert_array_equal(a, b)
+    h_ref, p_ref, _ = oracle.batch_sample(oracle.CAP, *_host(x, synth.PLANES))
+    eh, ep = _errors(results[0][:3], results[0][3], h_ref, p_ref)
+    assert eh.max() <= TOL_H and ep.max() <= TOL_PDF
+
+
+def test_determinism_and_chunking(env):
+    """Outputs are a pure function of the inputs: repeated calls, split calls
+    and different streams are bit-identical (vndf.h)."""
+    oracle, vndf, synth, dev = env
+    n = (1 << 20) + 5
+    x = synth.fill(2, 1, n, device=dev)
+    a = _stream_run(vndf, x, synth.PLANES)
+    s = torch.cuda.Stream(dev)
+    b = _stream_run(vndf, x, synth.PLANES, stream=s)
+    k = 333331
+    c = vndf.empty_outputs(n, dev)
+    vndf.vndf_sample_cap_pdf(*[x[p][:k] for p in synth.PLANES], *[t[:k] for t in c], n=k)
+    vndf.vndf_sample_cap_pdf(*[x[p][k:] for p in synth.PLANES], *[t[k:] for t in c], n=n - k)
+    torch.cuda.synchronize()
+    for u, v, w in zip(a, b, c):
+        assert torch.equal(u, v) and torch.equal(u, w)
+    # Philox chunking by first_index
+    m = 100003
+    p1 = vndf.empty_outputs(m, dev)
+    vndf.vndf_sample_cap_philox(3, 5000, m, *p1)
+    p2 = vndf.empty_outputs(m, dev)
+    vndf.vndf_sample_cap_philox(3, 5000, 40000, *[t[:40000] for t in p2])
+    vndf.vndf_sample_cap_philox(3, 45000, m - 40000, *[t[40000:] for t in p2])
+    torch.cuda.synchronize()
+    for u, v in zip(p1, p2):
+        assert torch.equal(u, v)
+
+
+def test_h_only_matches_h_pdf(env):
+    oracle, vndf, synth, dev = env
+    x = synth.fill(3, 2, 1 << 20, device=dev)
+    a = _stream_run(vndf, x, synth.PLANES, pdf=False)
+    b = _stream_run(vndf, x, synth.PLANES, pdf=True)
+    for u, v in zip(a, b[:3]):
+        assert torch.equal(u, v)
+
+
+@pytest.mark.parametrize("cid", [1, 2, 5])
+def test_heitz_baseline_conditioned_parity(env, cid):
+    """The literal fp32 Listing 2 baseline (reading R8): within the
+    contract on samples whose Listing-2 reprojection is well conditioned
+    (oracle ti >= 0.05, |m| >= 0.1 max(alpha)); the rest is reported."""
+    oracle, vndf, synth, dev = env
+    cfg = synth.CONFIGS[cid]
+    n = min(cfg.n, 1 << 22)
+    x = synth.fill(cfg.recipe, cfg.seed, n, device=dev)
+    out = _stream_run(vndf, x, synth.PLANES, pdf=True, kernel="heitz")
+    host = _host(x, synth.PLANES)
+    h_ref, p_ref, ti = oracle.batch_sample(oracle.HEITZ, *host)
+    eh, ep = _errors([o.cpu().numpy() for o in out[:3]], out[3].cpu().numpy(), h_ref, p_ref)
+    ax, ay = host[3].astype(np.float64), host[4].astype(np.float64)
+    s = np.where(host[2] < 0, -1.0, 1.0)
+    mt = np.sqrt((s * h_ref[0] / ax) ** 2 + (s * h_ref[1] / ay) ** 2 + h_ref[2] ** 2)
+    N = 1.0 / mt
+    good = (ti >= 0.05) & (N >= 0.1 * np.maximum(ax, ay))
+    assert good.mean() > 0.9
+    assert eh[good].max() <= TOL_H, float(eh[good].max())
+    assert ep[good].max() <= TOL_PDF, float(ep[good].max())
+    assert bool(torch.isfinite(out[0]).all())
+
+
+def test_host_entry_point_matches_device(env):
+    oracle, vndf, synth, dev = env
+    n = (1 << 23) + 17  # three pipeline chunks, ragged
+    x = synth.fill(5, 4, n, device=dev)
+    d = _stream_run(vndf, x, synth.PLANES)
+    hin = [x[k].cpu().pin_memory() for k in synth.PLANES]
+    hout = [torch.empty(n, dtype=torch.float32).pin_memory() for _ in range(4)]
+    vndf.vndf_sample_cap_pdf_host(*hin, *hout)
+    for a, b in zip(d, hout):
+        assert torch.equal(a.cpu(), b)
+    # pageable numpy buffers work too
+    nin = [t.numpy() for t in hin]
+    nout = [np.empty(n, dtype=np.float32) for _ in range(4)]
+    vndf.vndf_sample_cap_pdf_host(*nin, *nout)
+    for a, b in zip(d, nout):
+        np.testing.assert_array_equal(a.cpu().numpy(), b)
+
+
+def test_fixup_rates(env):
+    """The float64 fix-up stays rare (it is the accuracy safety net, DESIGN.md s.6)."""
+    oracle, vndf, synth, dev = env
+    for cid in (1, 2, 3, 5):
+        cfg = synth.CONFIGS[cid]
+        n = min(cfg.n, 1 << 24)
+        x = synth.fill(cfg.recipe, cfg.seed, n, device=dev)
+        c = torch.zeros(1, dtype=torch.int64, device=dev)
+        vndf.vndf_count_fixups(*[x[k] for k in synth.PLANES], c)
+        rate = int(c.item()) / n
+        print(f"config {cid}: fix-up rate {rate:.3e}")
+        assert rate < 0.02
+    c = torch.zeros(1, dtype=torch.int64, device=dev)
+    vndf.vndf_count_fixups_philox(3, 0, 1 << 24, c)
+    assert int(c.item()) / (1 << 24) < 0.02
+
+
+def test_error_codes(env):
+    oracle, vndf, synth, dev = env
+    L = vndf.lib()
+    import ctypes
+    x = synth.fill(1, 0, 64, device=dev)
+    o = vndf.empty_outputs(64, dev)
+    P = [ctypes.c_void_p(x[k].data_ptr()) for k in synth.PLANES]
+    Q = [ctypes.c_void_p(t.data_ptr()) for t in o]
+    assert L.vndf_sample_cap_pdf(*P, *Q, -1, None) == vndf.VNDF_ERR_INVALID_ARGUMENT
+    assert L.vndf_sample_cap_pdf(*P, *Q, 0, None) == vndf.VNDF_OK
+    assert L.vndf_sample_cap_pdf(*P[:6], None, *Q, 64, None) == vndf.VNDF_ERR_INVALID_ARGUMENT
+    assert L.vndf_sample_cap_pdf(*P, P[0], *Q[1:], 64, None) == vndf.VNDF_ERR_INVALID_ARGUMENT  # alias
+    assert L.vndf_sample_cap_pdf(*P, Q[0], Q[0], *Q[2:], 64, None) == vndf.VNDF_ERR_INVALID_ARGUMENT
+    assert L.vndf_sample_cap_pdf(*P, *Q[:3], None, 64, None) == vndf.VNDF_ERR_INVALID_ARGUMENT
+    odd = ctypes.c_void_p(x["u2"].data_ptr() + 2)
+    assert L.vndf_sample_cap_pdf(*P[:6], odd, *Q, 8, None) == vndf.VNDF_ERR_INVALID_ARGUMENT
+    assert L.vndf_sample_cap(*P, *Q[:3], 64, None) == vndf.VNDF_OK
+    assert L.vndf_sample_heitz2018(*P, *Q[:3], None, 64, None) == vndf.VNDF_OK
+    assert L.vndf_sample_cap_philox(1, 0, -5, *Q, None) == vndf.VNDF_ERR_INVALID_ARGUMENT
+    assert L.vndf_sample_cap_philox(1, 0, 64, Q[0], Q[0], Q[2], Q[3], None) == vndf.VNDF_ERR_INVALID_ARGUMENT
+    torch.cuda.synchronize()
