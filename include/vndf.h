@@ -124,15 +124,21 @@ vndf_status vndf_philox4x32_10(uint64_t seed, uint64_t first_index, int64_t n,
 
 /* End-to-end form of vndf_sample_cap_pdf on HOST buffers (pinned memory
  * recommended; pageable works but is slower).  Streams the batch through the
- * GPU in chunks, overlapping host->device copies, the kernel and
- * device->host copies on two streams; device staging is stream-ordered
- * (cudaMallocAsync) and released before return.  BLOCKING: returns when the
- * outputs are in host memory.  Work is ordered after prior work on `stream`. */
+ * GPU in chunks of 4 Mi samples, overlapping host->device copies, the kernel
+ * and device->host copies on two library-owned streams.  Device staging
+ * (2 x 4 Mi x 44 B = 369 MB per device) is allocated on first use and kept
+ * for later calls; vndf_release_host_staging() frees it.  BLOCKING: returns
+ * when the outputs are in host memory.  Work is ordered after prior work on
+ * `stream`. */
 vndf_status vndf_sample_cap_pdf_host(const float *wi_x, const float *wi_y, const float *wi_z,
                                      const float *alpha_x, const float *alpha_y,
                                      const float *u1, const float *u2,
                                      float *h_x, float *h_y, float *h_z, float *pdf,
                                      int64_t n, vndf_stream_t stream);
+
+/* Frees the cached staging of vndf_sample_cap_pdf_host on every device.
+ * VNDF_ERR_INVALID_ARGUMENT if a host call is in flight on another thread. */
+vndf_status vndf_release_host_staging(void);
 
 /* Diagnostic: number of samples the spherical-cap kernels would route to the
  * float64 recomputation for these inputs; ADDS the count to *count (device

@@ -26,7 +26,7 @@ VNDF_ERR_NOT_IMPLEMENTED = 3
 SYMBOLS = (
     "vndf_sample_cap", "vndf_sample_cap_pdf", "vndf_sample_heitz2018",
     "vndf_sample_cap_philox", "vndf_sample_heitz2018_philox", "vndf_philox4x32_10",
-    "vndf_sample_cap_pdf_host", "vndf_count_fixups", "vndf_count_fixups_philox",
+    "vndf_sample_cap_pdf_host", "vndf_release_host_staging", "vndf_count_fixups", "vndf_count_fixups_philox",
     "vndf_set_launch_config", "vndf_status_string", "vndf_last_cuda_error", "vndf_version",
 )
 
@@ -62,6 +62,7 @@ def lib() -> ctypes.CDLL:
         L.vndf_count_fixups.argtypes = [P] * 7 + [i64, P, P]
         L.vndf_count_fixups_philox.argtypes = [u64, u64, i64, P, P]
         L.vndf_set_launch_config.argtypes = [i32, i32, i32]
+        L.vndf_release_host_staging.argtypes = []
         L.vndf_status_string.argtypes = [i32]
         L.vndf_status_string.restype = ctypes.c_char_p
         L.vndf_last_cuda_error.argtypes = []
@@ -235,6 +236,10 @@ def vndf_sample_cap_pdf_host(wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, h_x, h_
     else:
         st = _stream(stream, None)
     _check("vndf_sample_cap_pdf_host", lib().vndf_sample_cap_pdf_host(*ptrs, n, st))
+
+
+def vndf_release_host_staging():
+    _check("vndf_release_host_staging", lib().vndf_release_host_staging())
 
 
 def vndf_set_launch_config(vector_width: int = 0, block_size: int = 0, blocks_per_sm: int = 0):

@@ -451,6 +451,82 @@ vndf_status launch_philox(uint64_t seed, uint64_t first, int64_t n, float* hx, f
               : launch_philox_v<METHOD, false, 1>(seed, first, n, hx, hy, hz, pdf, s);
 }
 
+// ------------------------------------------------ host-path staging cache --
+// The blocking host entry point streams a batch through two device staging
+// sets of kStagingChunk samples (11 planes each: 7 in, 4 out) on two streams.
+// One staging area per device is kept after first use (2 x 4 Mi x 44 B =
+// 369 MB) so repeated calls pay no allocation; a concurrent second caller on
+// the same device gets a private area that is freed when it returns.
+constexpr int64_t kStagingChunk = (int64_t)1 << 22;
+
+struct Staging {
+    int device = 0;
+    float* buf = nullptr;
+    cudaStream_t s[2] = {nullptr, nullptr};
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    bool busy = false;
+    bool cached = false;
+};
+std::map<int, Staging*> g_staging;
+
+cudaError_t destroy_staging(Staging* sg) {
+    cudaError_t first = cudaSuccess;
+    auto keep = [&](cudaError_t e) { if (first == cudaSuccess) first = e; };
+    for (auto x : sg->s)
+        if (x) keep(cudaStreamDestroy(x));
+    for (auto x : sg->ev)
+        if (x) keep(cudaEventDestroy(x));
+    if (sg->buf) keep(cudaFree(sg->buf));
+    delete sg;
+    return first;
+}
+
+cudaError_t create_staging(int dev, Staging** out) {
+    Staging* sg = new Staging();
+    sg->device = dev;
+    cudaError_t e = cudaMalloc((void**)&sg->buf, (size_t)2 * 11 * kStagingChunk * sizeof(float));
+    for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = cudaStreamCreateWithFlags(&sg->s[k], cudaStreamNonBlocking);
+    for (int k = 0; k < 3 && e == cudaSuccess; ++k) e = cudaEventCreateWithFlags(&sg->ev[k], cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+        destroy_staging(sg);
+        return e;
+    }
+    *out = sg;
+    return cudaSuccess;
+}
+
+cudaError_t acquire_staging(int dev, Staging** out) {
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        auto it = g_staging.find(dev);
+        if (it != g_staging.end() && !it->second->busy) {
+            it->second->busy = true;
+            *out = it->second;
+            return cudaSuccess;
+        }
+    }
+    Staging* sg = nullptr;
+    cudaError_t e = create_staging(dev, &sg);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(g_mu);
+    sg->busy = true;
+    if (g_staging.find(dev) == g_staging.end()) {
+        sg->cached = true;
+        g_staging[dev] = sg;
+    }
+    *out = sg;
+    return cudaSuccess;
+}
+
+void release_staging(Staging* sg) {
+    if (sg->cached) {
+        std::lock_guard<std::mutex> lk(g_mu);
+        sg->busy = false;
+        return;
+    }
+    destroy_staging(sg);
+}
+
 }  // namespace
 
 // ================================================================== C ABI ==
@@ -548,71 +624,59 @@ vndf_status vndf_sample_cap_pdf_host(const float* wi_x, const float* wi_y, const
     const StreamArgs host = make_args(wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, h_x, h_y, h_z, pdf);
     vndf_status st = validate_stream(host, true, n);
     if (st != VNDF_OK || n == 0) return st;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e);
+    Staging* sg = nullptr;
+    e = acquire_staging(dev, &sg);
+    if (e != cudaSuccess) return cuda_fail(e);
     cudaStream_t user = (cudaStream_t)stream;
-    const int64_t chunk = std::min<int64_t>(n, (int64_t)1 << 22);
-    const int nsets = 2;
-    const size_t set_floats = (size_t)chunk * 11;
-    float* dbuf = nullptr;
-    cudaStream_t ss[2] = {nullptr, nullptr};
-    cudaEvent_t ready = nullptr, done[2] = {nullptr, nullptr};
-    cudaError_t e = cudaSuccess;
     vndf_status result = VNDF_OK;
-#define VNDF_TRY(x)                 \
-    do {                            \
-        e = (x);                    \
-        if (e != cudaSuccess) goto fail; \
-    } while (0)
-    VNDF_TRY(cudaStreamCreateWithFlags(&ss[0], cudaStreamNonBlocking));
-    VNDF_TRY(cudaStreamCreateWithFlags(&ss[1], cudaStreamNonBlocking));
-    VNDF_TRY(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-    VNDF_TRY(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming));
-    VNDF_TRY(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming));
-    VNDF_TRY(cudaMallocAsync((void**)&dbuf, set_floats * nsets * sizeof(float), user));
-    VNDF_TRY(cudaEventRecord(ready, user));
-    VNDF_TRY(cudaStreamWaitEvent(ss[0], ready, 0));
-    VNDF_TRY(cudaStreamWaitEvent(ss[1], ready, 0));
-    for (int64_t off = 0, c = 0; off < n; off += chunk, ++c) {
-        const int64_t m = std::min<int64_t>(chunk, n - off);
-        cudaStream_t s = ss[c % 2];
-        float* base = dbuf + (size_t)(c % 2) * set_floats;
+    // order after prior work on the caller's stream
+    e = cudaEventRecord(sg->ev[0], user);
+    for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = cudaStreamWaitEvent(sg->s[k], sg->ev[0], 0);
+    const float* hin[7] = {wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2};
+    float* hout[4] = {h_x, h_y, h_z, pdf};
+    for (int64_t off = 0, c = 0; off < n && e == cudaSuccess && result == VNDF_OK; off += kStagingChunk, ++c) {
+        const int64_t m = std::min<int64_t>(kStagingChunk, n - off);
+        cudaStream_t s = sg->s[c % 2];
+        float* base = sg->buf + (size_t)(c % 2) * 11 * kStagingChunk;
         float* d[11];
-        for (int k = 0; k < 11; ++k) d[k] = base + (size_t)k * chunk;
-        const float* hin[7] = {wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2};
-        float* hout[4] = {h_x, h_y, h_z, pdf};
+        for (int k = 0; k < 11; ++k) d[k] = base + (size_t)k * kStagingChunk;
         const size_t bytes = (size_t)m * sizeof(float);
-        for (int k = 0; k < 7; ++k)
-            VNDF_TRY(cudaMemcpyAsync(d[k], hin[k] + off, bytes, cudaMemcpyHostToDevice, s));
+        for (int k = 0; k < 7 && e == cudaSuccess; ++k)
+            e = cudaMemcpyAsync(d[k], hin[k] + off, bytes, cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) break;
         const StreamArgs da = make_args(d[0], d[1], d[2], d[3], d[4], d[5], d[6], d[7], d[8], d[9], d[10]);
         result = launch_stream<kCap, true>(da, m, s);
-        if (result != VNDF_OK) goto fail_status;
-        for (int k = 0; k < 4; ++k)
-            VNDF_TRY(cudaMemcpyAsync(hout[k] + off, d[7 + k], bytes, cudaMemcpyDeviceToHost, s));
+        for (int k = 0; k < 4 && e == cudaSuccess && result == VNDF_OK; ++k)
+            e = cudaMemcpyAsync(hout[k] + off, d[7 + k], bytes, cudaMemcpyDeviceToHost, s);
     }
-    VNDF_TRY(cudaEventRecord(done[0], ss[0]));
-    VNDF_TRY(cudaEventRecord(done[1], ss[1]));
-    VNDF_TRY(cudaStreamWaitEvent(user, done[0], 0));
-    VNDF_TRY(cudaStreamWaitEvent(user, done[1], 0));
-    VNDF_TRY(cudaFreeAsync(dbuf, user));
-    dbuf = nullptr;
-    VNDF_TRY(cudaStreamSynchronize(user));
-    for (auto x : ss) cudaStreamDestroy(x);
-    cudaEventDestroy(ready);
-    for (auto x : done) cudaEventDestroy(x);
-    return VNDF_OK;
-#undef VNDF_TRY
-fail:
-    result = cuda_fail(e);
-fail_status:
-    if (ss[0]) cudaStreamSynchronize(ss[0]);
-    if (ss[1]) cudaStreamSynchronize(ss[1]);
-    if (dbuf) cudaFreeAsync(dbuf, user);
-    cudaStreamSynchronize(user);
-    for (auto x : ss)
-        if (x) cudaStreamDestroy(x);
-    if (ready) cudaEventDestroy(ready);
-    for (auto x : done)
-        if (x) cudaEventDestroy(x);
-    return result;
+    // join both pipeline streams back into the caller's stream, then block
+    for (int k = 0; k < 2; ++k) {
+        cudaEventRecord(sg->ev[1 + k], sg->s[k]);
+        cudaStreamWaitEvent(user, sg->ev[1 + k], 0);
+    }
+    const cudaError_t es = cudaStreamSynchronize(user);
+    if (e == cudaSuccess) e = es;
+    release_staging(sg);
+    if (result != VNDF_OK) return result;
+    return e == cudaSuccess ? VNDF_OK : cuda_fail(e);
+}
+
+vndf_status vndf_release_host_staging(void) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    cudaError_t first = cudaSuccess;
+    for (auto& kv : g_staging) {
+        Staging* sg = kv.second;
+        if (sg->busy) return VNDF_ERR_INVALID_ARGUMENT;
+    }
+    for (auto& kv : g_staging) {
+        cudaError_t e = destroy_staging(kv.second);
+        if (first == cudaSuccess) first = e;
+    }
+    g_staging.clear();
+    return first == cudaSuccess ? VNDF_OK : cuda_fail(first);
 }
 
 vndf_status vndf_set_launch_config(int vector_width, int block_size, int blocks_per_sm) {

@@ -22,16 +22,17 @@ constexpr double kPiD = 3.14159265358979323846;
 
 // ---------------------------------------------------------------------------
 // Conditioning flag thresholds ("error budget").
-// The fp32 half vector hs = c + ws carries an absolute error e ~ 2e-7 (fp32
-// rounding of O(1) terms plus sincospif's ulp).  The unstretch divides it by
+// The fp32 half vector hs = c + ws carries an absolute error e <~ 1e-6 (fp32
+// rounding of O(1) terms, MUFU sin/cos ~3.6e-7, and for the fused Philox path
+// the same again from generating wi with MUFU functions).  The unstretch divides it by
 // |m| = |diag(ax, ay, 1) hs| after multiplying it by at most max(ax, ay):
 // |dh| ~ e max(a) / |m|.  The pdf |m|^3 / (pi ax ay a |hs|^2) carries
 // ~3 e max(a)/|m| + 2 e/|hs| relative error.  Samples outside
 //     |m|^2 >= kFlagM * max(a)^2   and   |hs|^2 >= kFlagHs
 // are recomputed in float64.
 // ---------------------------------------------------------------------------
-constexpr float kFlagM = 4.0e-3f;   // |m| < 0.063 max(a)  -> |dh| ~> 3e-6
-constexpr float kFlagHs = 1.0e-3f;  // |hs| < 0.032         -> pdf rel ~> 1.2e-5
+constexpr float kFlagM = 1.0e-2f;   // |m| < 0.1 max(a): beyond, |dh| <~ 1e-5 e/1e-6
+constexpr float kFlagHs = 4.0e-3f;  // |hs| < 0.063:     beyond, pdf rel <~ 3e-5 e/1e-6
 
 // ---------------------------------------------------------------------------
 // Explicit single-instruction SFU approximations (MUFU.RSQ / SQRT / RCP).
@@ -52,10 +53,23 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return r;
 }
 
+__device__ __forceinline__ float ex2_approx(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 // sin(2 pi u), cos(2 pi u) for u in [0, 1): phi = 2 pi u1 (Listing 3,
-// Listing 2).  sincospif is accurate to ~1 ulp on the whole range.
+// Listing 2).  The argument is first reduced exactly to v = u - 1/2 in
+// [-1/2, 1/2) (exact for u in [0, 1) on the 2^-24 grid and for u >= 1/4
+// generally), so MUFU.SIN / MUFU.COS run on |2 pi v| <= pi where their
+// absolute error is ~2^-21.4; sin(2 pi u) = -sin(2 pi v), same for cos.
 __device__ __forceinline__ void sincos_2pi(float u, float* s, float* c) {
-    sincospif(2.0f * u, s, c);
+    const float v = u - 0.5f;
+    float sv, cv;
+    __sincosf(v * 6.28318530717958648f, &sv, &cv);
+    *s = -sv;
+    *c = -cv;
 }
 
 struct Sample {
@@ -228,15 +242,15 @@ struct Inputs {
 __device__ __forceinline__ Inputs c4_inputs_fp32(uint4 X, uint4 Y) {
     Inputs in;
     const float ua = u01f(X.x), ub = u01f(X.y);
-    const float r = sqrtf(ua * (2.0f - ua));   // IEEE sqrt: generation stays ~1 ulp
+    const float r = sqrt_approx(ua * (2.0f - ua));
     float sp, cp;
     sincos_2pi(ub, &sp, &cp);
     in.wx = r * cp;
     in.wy = r * sp;
     in.wz = 1.0f - ua;
     // 0.01 * 100^u = 2^((u - 1) log2 100); (u - 1) is exact
-    in.ax = exp2f((u01f(X.z) - 1.0f) * kLog2_100F);
-    in.ay = exp2f((u01f(X.w) - 1.0f) * kLog2_100F);
+    in.ax = ex2_approx(fmaf(u01f(X.z), kLog2_100F, -kLog2_100F));
+    in.ay = ex2_approx(fmaf(u01f(X.w), kLog2_100F, -kLog2_100F));
     in.u1 = u01f(Y.x);
     in.u2 = u01f(Y.y);
     return in;

@@ -251,7 +251,12 @@ def test_heitz_baseline_conditioned_parity(env, cid):
     s = np.where(host[2] < 0, -1.0, 1.0)
     mt = np.sqrt((s * h_ref[0] / ax) ** 2 + (s * h_ref[1] / ay) ** 2 + h_ref[2] ** 2)
     N = 1.0 / mt
-    good = (ti >= 0.05) & (N >= 0.1 * np.maximum(ax, ay))
+    # Listing 2 L445 takes sqrt(1 - t1^2) with t1 = sqrt(u2) cos(2 pi u1): ill
+    # conditioned at the rim of the disk, where it is multiplied by (1 - s)
+    rim = 1.0 - host[6].astype(np.float64) * np.cos(2 * np.pi * host[5].astype(np.float64)) ** 2
+    good = (ti >= 0.05) & (N >= 0.1 * np.maximum(ax, ay)) & (rim >= 2.5e-3)
+    print(f"config {cid}: Heitz conditioned subset {good.mean():.4f}; outside it max|dh| "
+          f"{eh[~good].max() if (~good).any() else 0:.2e}")
     assert good.mean() > 0.9
     assert eh[good].max() <= TOL_H, float(eh[good].max())
     assert ep[good].max() <= TOL_PDF, float(ep[good].max())
