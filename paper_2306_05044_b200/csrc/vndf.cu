@@ -102,29 +102,26 @@ __device__ __forceinline__ void st_stream<8>(float* p, const Vec<8>& r) {
 }
 
 // ------------------------------------------------------------ one sample --
+// fp32 sample; returns the conditioning flag (always false for Heitz).
 template <int METHOD, bool PDF>
-__device__ __forceinline__ Sample sample_one(float wx, float wy, float wz, float ax, float ay,
-                                             float u1, float u2) {
-    Sample o;
-    if (METHOD == kCap) {
-        const bool flag = cap_fp32<PDF>(wx, wy, wz, ax, ay, u1, u2, o);
-        if (__builtin_expect(flag, 0)) {
-            const float4 f = cap_fp64(wx, wy, wz, ax, ay, u1, u2);
-            o.x = f.x;
-            o.y = f.y;
-            o.z = f.z;
-            o.pdf = f.w;
-        }
-    } else {
-        heitz_fp32<PDF>(wx, wy, wz, ax, ay, u1, u2, o);
-    }
-    return o;
+__device__ __forceinline__ bool sample_one(float wx, float wy, float wz, float ax, float ay, float u1,
+                                           float u2, Sample& o) {
+    const float v1 = u1 - 0.5f;  // exact for u1 on the 2^-24 grid and for u1 >= 1/4
+    if (METHOD == kCap) return cap_fp32<PDF>(wx, wy, wz, ax, ay, v1, u2, 1.0f - u2, o);
+    heitz_fp32<PDF>(wx, wy, wz, ax, ay, v1, u2, o);
+    return false;
+}
+
+__device__ __forceinline__ void fix_one(const StreamArgs& a, bool pdf, int64_t i) {
+    cap_fix_stream(a.wx, a.wy, a.wz, a.ax, a.ay, a.u1, a.u2, a.hx, a.hy, a.hz, pdf ? a.pdf : nullptr, i);
 }
 
 // ------------------------------------------------------- streamed kernel --
 // Chunk c covers samples [c V, c V + V).  Full chunks go through the vector
 // path on a persistent grid-stride loop; the n mod V tail is done by the
-// first threads of the grid with scalar accesses.
+// first threads of the grid with scalar accesses.  Flagged samples of a
+// chunk are recomputed in float64 after the chunk's stores (in-thread
+// deferral: the vector loop itself stays call-free).
 template <int METHOD, bool PDF, int V>
 __global__ void __launch_bounds__(256) stream_kernel(StreamArgs a, int64_t n) {
     const int64_t nchunks = n / V;
@@ -137,10 +134,13 @@ __global__ void __launch_bounds__(256) stream_kernel(StreamArgs a, int64_t n) {
                      ay = ld_stream<V>(a.ay + i), u1 = ld_stream<V>(a.u1 + i),
                      u2 = ld_stream<V>(a.u2 + i);
         Vec<V> hx, hy, hz, pd;
+        unsigned flags = 0;
 #pragma unroll
         for (int j = 0; j < V; ++j) {
-            const Sample o = sample_one<METHOD, PDF>(wx.v[j], wy.v[j], wz.v[j], ax.v[j],
-                                                     ay.v[j], u1.v[j], u2.v[j]);
+            Sample o;
+            const bool f = sample_one<METHOD, PDF>(wx.v[j], wy.v[j], wz.v[j], ax.v[j], ay.v[j],
+                                                   u1.v[j], u2.v[j], o);
+            flags |= (unsigned)f << j;
             hx.v[j] = o.x;
             hy.v[j] = o.y;
             hz.v[j] = o.z;
@@ -150,46 +150,88 @@ __global__ void __launch_bounds__(256) stream_kernel(StreamArgs a, int64_t n) {
         st_stream<V>(a.hy + i, hy);
         st_stream<V>(a.hz + i, hz);
         if (PDF) st_stream<V>(a.pdf + i, pd);
+        if (METHOD == kCap && __builtin_expect(flags != 0, 0)) {
+            do {
+                const int j = __ffs(flags) - 1;
+                flags &= flags - 1;
+                fix_one(a, PDF, i + j);
+            } while (flags);
+        }
     }
     if (V > 1) {
         const int64_t i = nchunks * V + tid;
         if (i < n) {
-            const Sample o = sample_one<METHOD, PDF>(a.wx[i], a.wy[i], a.wz[i], a.ax[i], a.ay[i],
-                                                     a.u1[i], a.u2[i]);
+            Sample o;
+            const bool f = sample_one<METHOD, PDF>(a.wx[i], a.wy[i], a.wz[i], a.ax[i], a.ay[i],
+                                                   a.u1[i], a.u2[i], o);
             a.hx[i] = o.x;
             a.hy[i] = o.y;
             a.hz[i] = o.z;
             if (PDF) a.pdf[i] = o.pdf;
+            if (METHOD == kCap && f) fix_one(a, PDF, i);
         }
     }
 }
 
 // ----------------------------------------------------- fused Philox kernel --
+// Deferred float64 fix-up queue of the fused kernel (compute-bound: inline
+// fp64 work would diverge the warp).  Flagged local indices are appended with
+// one atomic each (~0.4% of samples); a second kernel recomputes them with all
+// lanes busy.  An index beyond the capacity is fixed inline (correct, slower).
+struct FixQueue {
+    unsigned long long* count;
+    uint64_t* idx;
+    uint64_t cap;
+};
+
 template <int METHOD, bool PDF>
-__device__ __forceinline__ Sample philox_one(uint64_t seed, uint64_t gi) {
+__device__ __forceinline__ Sample philox_one(uint64_t seed, uint64_t first, uint64_t k,
+                                             const FixQueue& fq) {
     uint4 X, Y;
-    philox_xy(seed, gi, X, Y);
+    philox_xy(seed, first + k, X, Y);
     const Inputs in = c4_inputs_fp32(X, Y);
     Sample o;
     if (METHOD == kCap) {
-        const bool flag = cap_fp32<PDF>(in.wx, in.wy, in.wz, in.ax, in.ay, in.u1, in.u2, o);
+        // config-4 inputs are on the upper hemisphere (wi.z = 1 - u > 0): no flip
+        const bool flag = cap_fp32<PDF, false>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o);
         if (__builtin_expect(flag, 0)) {
-            const float4 f = cap_philox_fp64(seed, gi);
-            o.x = f.x;
-            o.y = f.y;
-            o.z = f.z;
-            o.pdf = f.w;
+            const unsigned long long slot = atomicAdd(fq.count, 1ull);
+            if (slot < fq.cap) {
+                fq.idx[slot] = k;
+            } else {
+                const float4 f = cap_philox_fp64(seed, first + k);
+                o.x = f.x;
+                o.y = f.y;
+                o.z = f.z;
+                o.pdf = f.w;
+            }
         }
     } else {
-        heitz_fp32<PDF>(in.wx, in.wy, in.wz, in.ax, in.ay, in.u1, in.u2, o);
+        heitz_fp32<PDF, false>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, o);
     }
     return o;
+}
+
+__global__ void __launch_bounds__(128) philox_fixup_kernel(uint64_t seed, uint64_t first, FixQueue fq,
+                                                            float* __restrict__ hx, float* __restrict__ hy,
+                                                            float* __restrict__ hz, float* __restrict__ pdf) {
+    const uint64_t m = min((uint64_t)*fq.count, fq.cap);
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < m;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = fq.idx[t];
+        const float4 f = cap_philox_fp64(seed, first + k);
+        hx[k] = f.x;
+        hy[k] = f.y;
+        hz[k] = f.z;
+        if (pdf) pdf[k] = f.w;
+    }
 }
 
 template <int METHOD, bool PDF, int V>
 __global__ void __launch_bounds__(256) philox_kernel(uint64_t seed, uint64_t first, int64_t n,
                                                      float* __restrict__ hxp, float* __restrict__ hyp,
-                                                     float* __restrict__ hzp, float* __restrict__ pdfp) {
+                                                     float* __restrict__ hzp, float* __restrict__ pdfp,
+                                                     FixQueue fq) {
     const int64_t nchunks = n / V;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -198,7 +240,7 @@ __global__ void __launch_bounds__(256) philox_kernel(uint64_t seed, uint64_t fir
         Vec<V> hx, hy, hz, pd;
 #pragma unroll
         for (int j = 0; j < V; ++j) {
-            const Sample o = philox_one<METHOD, PDF>(seed, first + (uint64_t)(i + j));
+            const Sample o = philox_one<METHOD, PDF>(seed, first, (uint64_t)(i + j), fq);
             hx.v[j] = o.x;
             hy.v[j] = o.y;
             hz.v[j] = o.z;
@@ -212,7 +254,7 @@ __global__ void __launch_bounds__(256) philox_kernel(uint64_t seed, uint64_t fir
     if (V > 1) {
         const int64_t i = nchunks * V + tid;
         if (i < n) {
-            const Sample o = philox_one<METHOD, PDF>(seed, first + (uint64_t)i);
+            const Sample o = philox_one<METHOD, PDF>(seed, first, (uint64_t)i, fq);
             hxp[i] = o.x;
             hyp[i] = o.y;
             hzp[i] = o.z;
@@ -247,7 +289,9 @@ __global__ void __launch_bounds__(256) count_stream_kernel(StreamArgs a, int64_t
         bool flag = false;
         if (i < n) {
             Sample o;
-            flag = cap_fp32<true>(a.wx[i], a.wy[i], a.wz[i], a.ax[i], a.ay[i], a.u1[i], a.u2[i], o);
+            const float u2 = a.u2[i];
+            flag = cap_fp32<true>(a.wx[i], a.wy[i], a.wz[i], a.ax[i], a.ay[i], a.u1[i] - 0.5f, u2,
+                                  1.0f - u2, o);
         }
         warp_count(flag, count);
     }
@@ -266,7 +310,7 @@ __global__ void __launch_bounds__(256) count_philox_kernel(uint64_t seed, uint64
             philox_xy(seed, first + (uint64_t)i, X, Y);
             const Inputs in = c4_inputs_fp32(X, Y);
             Sample o;
-            flag = cap_fp32<true>(in.wx, in.wy, in.wz, in.ax, in.ay, in.u1, in.u2, o);
+            flag = cap_fp32<true>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o);
         }
         warp_count(flag, count);
     }
@@ -431,8 +475,34 @@ vndf_status launch_philox_v(uint64_t seed, uint64_t first, int64_t n, float* hx,
     int grid = 0;
     cudaError_t e = grid_for(k, block, std::max<int64_t>(n / V, 1), &grid);
     if (e != cudaSuccess) return cuda_fail(e);
-    philox_kernel<METHOD, PDF, V><<<grid, block, 0, s>>>(seed, first, n, hx, hy, hz, pdf);
+    FixQueue fq{nullptr, nullptr, 0};
+    void* qbuf = nullptr;
+    if (METHOD == kCap) {
+        // stream-ordered transient queue: [count | cap indices]
+        fq.cap = (uint64_t)std::min<int64_t>(std::max<int64_t>(n / 128, 1 << 16), (int64_t)1 << 26);
+        e = cudaMallocAsync(&qbuf, sizeof(unsigned long long) + fq.cap * sizeof(uint64_t), s);
+        if (e != cudaSuccess) return cuda_fail(e);
+        fq.count = (unsigned long long*)qbuf;
+        fq.idx = (uint64_t*)((char*)qbuf + sizeof(unsigned long long));
+        e = cudaMemsetAsync(fq.count, 0, sizeof(unsigned long long), s);
+        if (e != cudaSuccess) {
+            cudaFreeAsync(qbuf, s);
+            return cuda_fail(e);
+        }
+    }
+    philox_kernel<METHOD, PDF, V><<<grid, block, 0, s>>>(seed, first, n, hx, hy, hz, pdf, fq);
     e = cudaGetLastError();
+    if (e == cudaSuccess && METHOD == kCap) {
+        int sms = 0, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        philox_fixup_kernel<<<std::max(sms, 1) * 4, 128, 0, s>>>(seed, first, fq, hx, hy, hz, pdf);
+        e = cudaGetLastError();
+    }
+    if (qbuf) {
+        const cudaError_t ef = cudaFreeAsync(qbuf, s);
+        if (e == cudaSuccess) e = ef;
+    }
     return e == cudaSuccess ? VNDF_OK : cuda_fail(e);
 }
 

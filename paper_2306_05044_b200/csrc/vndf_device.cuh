@@ -60,12 +60,11 @@ __device__ __forceinline__ float ex2_approx(float x) {
 }
 
 // sin(2 pi u), cos(2 pi u) for u in [0, 1): phi = 2 pi u1 (Listing 3,
-// Listing 2).  The argument is first reduced exactly to v = u - 1/2 in
-// [-1/2, 1/2) (exact for u in [0, 1) on the 2^-24 grid and for u >= 1/4
+// Listing 2).  Callers pass the exactly reduced v = u - 1/2 in
+// [-1/2, 1/2) (exact on the 2^-24 grid of the uniforms, and for u >= 1/4
 // generally), so MUFU.SIN / MUFU.COS run on |2 pi v| <= pi where their
 // absolute error is ~2^-21.4; sin(2 pi u) = -sin(2 pi v), same for cos.
-__device__ __forceinline__ void sincos_2pi(float u, float* s, float* c) {
-    const float v = u - 0.5f;
+__device__ __forceinline__ void sincos_2pi_reduced(float v, float* s, float* c) {
     float sv, cv;
     __sincosf(v * 6.28318530717958648f, &sv, &cv);
     *s = -sv;
@@ -90,10 +89,13 @@ struct Sample {
 //   D_vis = 2 (hs.ws) |m|^3 / (pi a ax ay |hs|^4) = |m|^3 / (pi a ax ay |hs|^2),
 //   m = diag(ax, ay, 1) hs (the unnormalised output).
 // ---------------------------------------------------------------------------
-template <bool PDF>
+// v1 = u1 - 1/2 and q = 1 - u2 are passed precomputed (they are free when the
+// uniforms are generated in-kernel from integer words).  FLIP = false drops
+// the below-horizon handling for inputs known to have wi.z >= 0 (config 4).
+template <bool PDF, bool FLIP = true>
 __device__ __forceinline__ bool cap_fp32(float wx, float wy, float wz, float ax, float ay,
-                                         float u1, float u2, Sample& o) {
-    const float s = (wz < 0.0f) ? -1.0f : 1.0f;           // reading R4 (flip)
+                                         float v1, float u2, float q, Sample& o) {
+    const float s = (FLIP && wz < 0.0f) ? -1.0f : 1.0f;  // reading R4 (flip)
     // (1) warp to the hemisphere configuration: ws = M^-1 w / |M^-1 w|
     const float tx = ax * wx, ty = ay * wy;
     const float L2 = fmaf(tx, tx, fmaf(ty, ty, wz * wz));
@@ -101,13 +103,12 @@ __device__ __forceinline__ bool cap_fp32(float wx, float wy, float wz, float ax,
     const float wsx = tx * sinvL, wsy = ty * sinvL, wsz = wz * sinvL;
     // (2) sample the spherical cap z in (-ws.z, 1], phi = 2 pi u1
     const float a = 1.0f + wsz;
-    const float q = 1.0f - u2;
     const float hz = q * a;
     const float rs2 = fmaf(wsx, wsx, wsy * wsy);
     const float sin2 = u2 * fmaf(hz, a, rs2);
     const float st = sqrt_approx(sin2);
     float sp, cp;
-    sincos_2pi(u1, &sp, &cp);
+    sincos_2pi_reduced(v1, &sp, &cp);
     // half vector hs = c + ws, not normalised
     const float hx = fmaf(st, cp, wsx), hy = fmaf(st, sp, wsy);
     // (3) warp back with M^-T = diag(ax, ay, 1) and normalise
@@ -132,8 +133,8 @@ __device__ __forceinline__ bool cap_fp32(float wx, float wy, float wz, float ax,
 // Float64 recomputation of one cap sample (the fix-up).  Same algebra as
 // cap_fp32, IEEE double throughout (sincospi, sqrt, division).
 // ---------------------------------------------------------------------------
-__device__ __noinline__ float4 cap_fp64(double wx, double wy, double wz, double ax, double ay,
-                                        double u1, double u2) {
+__device__ __forceinline__ float4 cap_fp64_d(double wx, double wy, double wz, double ax, double ay,
+                                             double u1, double u2) {
     const double s = (wz < 0.0) ? -1.0 : 1.0;
     const double tx = ax * wx, ty = ay * wy;
     const double L = sqrt(tx * tx + ty * ty + wz * wz);
@@ -154,16 +155,39 @@ __device__ __noinline__ float4 cap_fp64(double wx, double wy, double wz, double 
     return make_float4((float)(s * mx / N), (float)(s * my / N), (float)(s * hz / N), (float)pdf);
 }
 
+// Out-of-line entry for the streamed kernels: widening happens in here, so the
+// fp32 hot path carries no conversions for it.
+__device__ __noinline__ float4 cap_fp64(float wx, float wy, float wz, float ax, float ay, float u1,
+                                        float u2) {
+    return cap_fp64_d(wx, wy, wz, ax, ay, u1, u2);
+}
+
+// Streamed fix-up of sample i: re-reads its inputs (L2-resident: the chunk was
+// just loaded), recomputes in float64 and overwrites the fp32 outputs.  Called
+// after the chunk's vector stores, so the hot loop keeps no values live across
+// the call.
+__device__ __noinline__ void cap_fix_stream(const float* __restrict__ wx, const float* __restrict__ wy,
+                                            const float* __restrict__ wz, const float* __restrict__ ax,
+                                            const float* __restrict__ ay, const float* __restrict__ u1,
+                                            const float* __restrict__ u2, float* hx, float* hy,
+                                            float* hz, float* pdf, int64_t i) {
+    const float4 f = cap_fp64_d(wx[i], wy[i], wz[i], ax[i], ay[i], u1[i], u2[i]);
+    hx[i] = f.x;
+    hy[i] = f.y;
+    hz[i] = f.z;
+    if (pdf) pdf[i] = f.w;
+}
+
 // ---------------------------------------------------------------------------
 // Heitz-2018 baseline, fp32: Listing 1 around Listing 2 taken
 // literally, with the same SFU primitives as the cap kernel.
 // pdf: Eq. 1 for a unit std-space normal hs:
 //   D_vis = 2 max(hs.ws, 0) |m|^3 / (pi a ax ay |hs|^4).
 // ---------------------------------------------------------------------------
-template <bool PDF>
+template <bool PDF, bool FLIP = true>
 __device__ __forceinline__ void heitz_fp32(float wx, float wy, float wz, float ax, float ay,
-                                           float u1, float u2, Sample& o) {
-    const float s = (wz < 0.0f) ? -1.0f : 1.0f;
+                                           float v1, float u2, Sample& o) {
+    const float s = (FLIP && wz < 0.0f) ? -1.0f : 1.0f;
     const float tx = ax * wx, ty = ay * wy;
     const float L2 = fmaf(tx, tx, fmaf(ty, ty, wz * wz));
     const float sinvL = s * rsqrt_approx(L2);
@@ -180,7 +204,7 @@ __device__ __forceinline__ void heitz_fp32(float wx, float wy, float wz, float a
     const float w2x = -wsz * w1y, w2y = wsz * w1x, w2z = wsx * w1y - wsy * w1x;
     // parameterization of the cross section
     float sp, cp;
-    sincos_2pi(u1, &sp, &cp);
+    sincos_2pi_reduced(v1, &sp, &cp);
     const float r = sqrt_approx(u2);
     const float t1 = r * cp;
     float t2 = r * sp;
@@ -211,22 +235,25 @@ __device__ __forceinline__ void heitz_fp32(float wx, float wy, float wz, float a
 // ---------------------------------------------------------------------------
 // Philox4x32-10 (Salmon et al. SC'11), counter-based: no state, any index.
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ void mul_hilo(uint32_t a, uint32_t b, uint32_t& hi, uint32_t& lo) {
+    uint64_t p;
+    asm("mul.wide.u32 %0, %1, %2;" : "=l"(p) : "r"(a), "r"(b));
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(p));
+}
+
 __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
 #pragma unroll
     for (int r = 0; r < 10; ++r) {
-        const uint64_t p0 = (uint64_t)0xD2511F53u * c.x;
-        const uint64_t p1 = (uint64_t)0xCD9E8D57u * c.z;
-        c = make_uint4((uint32_t)(p1 >> 32) ^ c.y ^ k.x, (uint32_t)p1,
-                       (uint32_t)(p0 >> 32) ^ c.w ^ k.y, (uint32_t)p0);
+        uint32_t hi0, lo0, hi1, lo1;
+        mul_hilo(0xD2511F53u, c.x, hi0, lo0);
+        mul_hilo(0xCD9E8D57u, c.z, hi1, lo1);
+        c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
         k.x += 0x9E3779B9u;
         k.y += 0xBB67AE85u;
     }
     return c;
 }
 
-__device__ __forceinline__ float u01f(uint32_t w) {
-    return __uint2float_rn(w >> 8) * 0x1p-24f;
-}
 __device__ __forceinline__ double u01d(uint32_t w) {
     return (double)(w >> 8) * 0x1p-24;
 }
@@ -235,24 +262,33 @@ __device__ __forceinline__ double u01d(uint32_t w) {
 constexpr float kLog2_100F = 6.64385618977472436f;
 constexpr double kLog2_100D = 6.64385618977472436;
 
+// Inputs of one sample in the form the samplers take: v1 = u1 - 1/2 and
+// q = 1 - u2 (both exact).
 struct Inputs {
-    float wx, wy, wz, ax, ay, u1, u2;
+    float wx, wy, wz, ax, ay, v1, u2, q;
 };
+
+// The 24-bit integer of a word, as float: u(w) = fw(w) 2^-24 exactly.
+__device__ __forceinline__ float fw(uint32_t w) { return __uint2float_rn(w >> 8); }
 
 __device__ __forceinline__ Inputs c4_inputs_fp32(uint4 X, uint4 Y) {
     Inputs in;
-    const float ua = u01f(X.x), ub = u01f(X.y);
-    const float r = sqrt_approx(ua * (2.0f - ua));
+    const float fa = fw(X.x);
+    const float ua = fa * 0x1p-24f;
+    const float z = fmaf(fa, -0x1p-24f, 1.0f);          // 1 - u(X0), exact
+    const float r = sqrt_approx(ua * (1.0f + z));       // sqrt(u (2 - u))
     float sp, cp;
-    sincos_2pi(ub, &sp, &cp);
+    sincos_2pi_reduced(fmaf(fw(X.y), 0x1p-24f, -0.5f), &sp, &cp);
     in.wx = r * cp;
     in.wy = r * sp;
-    in.wz = 1.0f - ua;
-    // 0.01 * 100^u = 2^((u - 1) log2 100); (u - 1) is exact
-    in.ax = ex2_approx(fmaf(u01f(X.z), kLog2_100F, -kLog2_100F));
-    in.ay = ex2_approx(fmaf(u01f(X.w), kLog2_100F, -kLog2_100F));
-    in.u1 = u01f(Y.x);
-    in.u2 = u01f(Y.y);
+    in.wz = z;
+    // 0.01 * 100^u = 2^((u - 1) log2 100); u log2 100 = fw (2^-24 log2 100) exactly
+    in.ax = ex2_approx(fmaf(fw(X.z), kLog2_100F * 0x1p-24f, -kLog2_100F));
+    in.ay = ex2_approx(fmaf(fw(X.w), kLog2_100F * 0x1p-24f, -kLog2_100F));
+    in.v1 = fmaf(fw(Y.x), 0x1p-24f, -0.5f);
+    const float f2 = fw(Y.y);
+    in.u2 = f2 * 0x1p-24f;
+    in.q = fmaf(f2, -0x1p-24f, 1.0f);
     return in;
 }
 
@@ -273,7 +309,7 @@ __device__ __noinline__ float4 cap_philox_fp64(uint64_t seed, uint64_t i) {
     sincospi(2.0 * ub, &sp, &cp);
     const double ax = exp2((u01d(X.z) - 1.0) * kLog2_100D);
     const double ay = exp2((u01d(X.w) - 1.0) * kLog2_100D);
-    return cap_fp64(r * cp, r * sp, 1.0 - ua, ax, ay, u01d(Y.x), u01d(Y.y));
+    return cap_fp64_d(r * cp, r * sp, 1.0 - ua, ax, ay, u01d(Y.x), u01d(Y.y));
 }
 
 }  // namespace vndf

@@ -1,0 +1,41 @@
+"""Small driver for ncu captures: a few launches of each hot kernel.
+
+python tools/prof_kernels.py [which]   which in {all, c2, c3, c4, c5}
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_2306_05044_b200 as vndf  # noqa: E402
+import synth  # noqa: E402
+
+which = sys.argv[1] if len(sys.argv) > 1 else "all"
+dev = torch.device("cuda:0")
+for cid in (2, 3, 5):
+    if which not in ("all", f"c{cid}"):
+        continue
+    cfg = synth.CONFIGS[cid]
+    x = synth.fill(cfg.recipe, cfg.seed, cfg.n, device=dev)
+    ins = [x[k] for k in synth.PLANES]
+    out = vndf.empty_outputs(cfg.n, dev, pdf=cfg.pdf)
+    for _ in range(2):
+        if cfg.pdf:
+            vndf.vndf_sample_cap_pdf(*ins, *out)
+            vndf.vndf_sample_heitz2018(*ins, *out)
+        else:
+            vndf.vndf_sample_cap(*ins, *out)
+            vndf.vndf_sample_heitz2018(*ins, *out, None)
+    torch.cuda.synchronize()
+    del x, ins, out
+if which in ("all", "c4"):
+    n = 1 << 26
+    o = vndf.empty_outputs(n, dev)
+    for _ in range(2):
+        vndf.vndf_sample_cap_philox(3, 0, n, *o)
+        vndf.vndf_sample_heitz2018_philox(3, 0, n, *o)
+    torch.cuda.synchronize()
+print("ok")
