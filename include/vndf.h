@@ -99,14 +99,15 @@ vndf_status vndf_sample_heitz2018(const float *wi_x, const float *wi_y, const fl
                                   float *h_x, float *h_y, float *h_z, float *pdf,
                                   int64_t n, vndf_stream_t stream);
 
-/* Fused in-kernel Philox4x32-10 (BASELINE config 4).  Sample k of the call
- * has global index i = first_index + k; its inputs are generated from
- * X = Philox(counter (i_lo, i_hi, 0, 0), key (seed_lo, seed_hi)) and
- * Y = Philox(counter (i_lo, i_hi, 1, 0), same key), u(w) = (w >> 8) 2^-24:
- *   wi uniform on the upper hemisphere: z = 1 - u(X0),
- *      r = sqrt(u(X0) (2 - u(X0))), phi = 2 pi u(X1);
- *   alpha_x = 0.01 * 100^u(X2), alpha_y = 0.01 * 100^u(X3);
- *   u1 = u(Y0), u2 = u(Y1).
+/* Fused in-kernel Philox4x32-10 (BASELINE config 4: key = seed, counter =
+ * sample index).  Sample k of the call has global index i = first_index + k
+ * and ONE Philox block W = Philox(counter (i_lo, i_hi, 0, 0), key (seed_lo,
+ * seed_hi)); u(w) = (w >> 8) 2^-24.  Its 128 bits give
+ *   u1 = u(W0), u2 = u(W1);
+ *   alpha_x = 0.01 * 100^u(W2), alpha_y = 0.01 * 100^u(W3);
+ *   wi uniform on the upper hemisphere from 16-bit uniforms
+ *      ua = (W0[7:0] | W1[7:0] << 8) 2^-16, ub = (W2[7:0] | W3[7:0] << 8) 2^-16:
+ *      z = 1 - ua, r = sqrt(ua (2 - ua)), phi = 2 pi ub.
  * Outputs h and pdf (16 B per sample); pdf may be NULL. */
 vndf_status vndf_sample_cap_philox(uint64_t seed, uint64_t first_index, int64_t n,
                                    float *h_x, float *h_y, float *h_z, float *pdf,

@@ -312,28 +312,31 @@ uint64_t orc_sample_raycast(const double wi_in[3], double ax, double ay,
 
 /* ------------------------------------------------------------------------ */
 /* Config-4 input recipe (DESIGN.md s.5), in float64 from the exact         */
-/* Philox uniforms: X = block 0, Y = block 1 of sample index i.             */
-/*   wi uniform on the upper hemisphere: z = 1 - u(X0),                     */
-/*      r = sqrt(u(X0) (2 - u(X0))), phi = 2 pi u(X1)                       */
-/*   ax = 0.01 * 100^u(X2), ay = 0.01 * 100^u(X3)  (log-uniform [0.01, 1])  */
-/*   u1 = u(Y0), u2 = u(Y1)                                                 */
+/* integers of ONE Philox block per sample: W = Philox(counter (i_lo, i_hi,  */
+/* 0, 0), key (seed_lo, seed_hi)) -- "key=seed, counter=sample index"       */
+/* (BASELINE.json config 4).  Bit split of the 128 bits:                    */
+/*   u1 = u(W0), u2 = u(W1)                 (24 bits each, the method's u)  */
+/*   ax = 0.01 * 100^u(W2), ay = 0.01 * 100^u(W3)   (log-uniform [0.01, 1]) */
+/*   ua = (W0[7:0] | W1[7:0] << 8) / 2^16, ub = (W2[7:0] | W3[7:0] << 8) / 2^16 */
+/*   wi uniform on the upper hemisphere: z = 1 - ua, r = sqrt(ua (2 - ua)), */
+/*      phi = 2 pi ub                                                       */
 /* ------------------------------------------------------------------------ */
 void orc_c4_inputs(uint64_t seed, uint64_t index, double out[7])
 {
-    uint32_t X[4], Y[4];
-    orc_philox_block(seed, index, 0u, X);
-    orc_philox_block(seed, index, 1u, Y);
-    double ua = orc_u01(X[0]), ub = orc_u01(X[1]);
+    uint32_t W[4];
+    orc_philox_block(seed, index, 0u, W);
+    double ua = (double)((W[0] & 0xFFu) | ((W[1] & 0xFFu) << 8)) / 65536.0;
+    double ub = (double)((W[2] & 0xFFu) | ((W[3] & 0xFFu) << 8)) / 65536.0;
     double z = 1.0 - ua;
     double r = sqrt(ua * (2.0 - ua));
     double phi = 2.0 * ORC_PI * ub;
     out[0] = r * cos(phi);
     out[1] = r * sin(phi);
     out[2] = z;
-    out[3] = 0.01 * pow(100.0, orc_u01(X[2]));
-    out[4] = 0.01 * pow(100.0, orc_u01(X[3]));
-    out[5] = orc_u01(Y[0]);
-    out[6] = orc_u01(Y[1]);
+    out[3] = 0.01 * pow(100.0, orc_u01(W[2]));
+    out[4] = 0.01 * pow(100.0, orc_u01(W[3]));
+    out[5] = orc_u01(W[0]);
+    out[6] = orc_u01(W[1]);
 }
 
 /* ------------------------------------------------------------------------ */

@@ -63,6 +63,12 @@ __device__ __forceinline__ Vec<1> ld_stream<1>(const float* p) {
     return r;
 }
 template <>
+__device__ __forceinline__ Vec<2> ld_stream<2>(const float* p) {
+    Vec<2> r;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0,%1}, [%2];" : "=f"(r.v[0]), "=f"(r.v[1]) : "l"(p));
+    return r;
+}
+template <>
 __device__ __forceinline__ Vec<4> ld_stream<4>(const float* p) {
     Vec<4> r;
     asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
@@ -86,6 +92,10 @@ __device__ __forceinline__ void st_stream(float* p, const Vec<V>& r);
 template <>
 __device__ __forceinline__ void st_stream<1>(float* p, const Vec<1>& r) {
     asm volatile("st.global.L1::no_allocate.f32 [%0], %1;" ::"l"(p), "f"(r.v[0]) : "memory");
+}
+template <>
+__device__ __forceinline__ void st_stream<2>(float* p, const Vec<2>& r) {
+    asm volatile("st.global.L1::no_allocate.v2.f32 [%0], {%1,%2};" ::"l"(p), "f"(r.v[0]), "f"(r.v[1]) : "memory");
 }
 template <>
 __device__ __forceinline__ void st_stream<4>(float* p, const Vec<4>& r) {
@@ -175,9 +185,11 @@ __global__ void __launch_bounds__(256) stream_kernel(StreamArgs a, int64_t n) {
 
 // ----------------------------------------------------- fused Philox kernel --
 // Deferred float64 fix-up queue of the fused kernel (compute-bound: inline
-// fp64 work would diverge the warp).  Flagged local indices are appended with
-// one atomic each (~0.4% of samples); a second kernel recomputes them with all
-// lanes busy.  An index beyond the capacity is fixed inline (correct, slower).
+// fp64 work would diverge the warp and its call would inflate the register
+// allocation).  Flagged local indices are appended with one (warp-aggregated)
+// atomic each (~0.4% of samples); a second kernel recomputes them with all
+// lanes busy.  If the queue overflowed (count > cap), the fix-up kernel
+// rescans every sample's flag instead: always correct, slower only then.
 struct FixQueue {
     unsigned long long* count;
     uint64_t* idx;
@@ -187,24 +199,14 @@ struct FixQueue {
 template <int METHOD, bool PDF>
 __device__ __forceinline__ Sample philox_one(uint64_t seed, uint64_t first, uint64_t k,
                                              const FixQueue& fq) {
-    uint4 X, Y;
-    philox_xy(seed, first + k, X, Y);
-    const Inputs in = c4_inputs_fp32(X, Y);
+    const Inputs in = c4_inputs_fp32(philox_sample(seed, first + k));
     Sample o;
     if (METHOD == kCap) {
         // config-4 inputs are on the upper hemisphere (wi.z = 1 - u > 0): no flip
         const bool flag = cap_fp32<PDF, false>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o);
         if (__builtin_expect(flag, 0)) {
             const unsigned long long slot = atomicAdd(fq.count, 1ull);
-            if (slot < fq.cap) {
-                fq.idx[slot] = k;
-            } else {
-                const float4 f = cap_philox_fp64(seed, first + k);
-                o.x = f.x;
-                o.y = f.y;
-                o.z = f.z;
-                o.pdf = f.w;
-            }
+            if (slot < fq.cap) fq.idx[slot] = k;
         }
     } else {
         heitz_fp32<PDF, false>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, o);
@@ -212,23 +214,46 @@ __device__ __forceinline__ Sample philox_one(uint64_t seed, uint64_t first, uint
     return o;
 }
 
-__global__ void __launch_bounds__(128) philox_fixup_kernel(uint64_t seed, uint64_t first, FixQueue fq,
-                                                            float* __restrict__ hx, float* __restrict__ hy,
-                                                            float* __restrict__ hz, float* __restrict__ pdf) {
-    const uint64_t m = min((uint64_t)*fq.count, fq.cap);
-    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < m;
-         t += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t k = fq.idx[t];
-        const float4 f = cap_philox_fp64(seed, first + k);
-        hx[k] = f.x;
-        hy[k] = f.y;
-        hz[k] = f.z;
-        if (pdf) pdf[k] = f.w;
+__global__ void __launch_bounds__(128) philox_fixup_kernel(uint64_t seed, uint64_t first, int64_t n,
+                                                            FixQueue fq, float* __restrict__ hx,
+                                                            float* __restrict__ hy, float* __restrict__ hz,
+                                                            float* __restrict__ pdf) {
+    const uint64_t count = *fq.count;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (count <= fq.cap) {
+        for (uint64_t t = t0; t < count; t += stride) {
+            const uint64_t k = fq.idx[t];
+            const float4 f = cap_philox_fp64(seed, first + k);
+            hx[k] = f.x;
+            hy[k] = f.y;
+            hz[k] = f.z;
+            if (pdf) pdf[k] = f.w;
+        }
+        return;
+    }
+    for (uint64_t k = t0; k < (uint64_t)n; k += stride) {  // overflow: rescan
+        const Inputs in = c4_inputs_fp32(philox_sample(seed, first + k));
+        Sample o;
+        if (cap_fp32<true, false>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o)) {
+            const float4 f = cap_philox_fp64(seed, first + k);
+            hx[k] = f.x;
+            hy[k] = f.y;
+            hz[k] = f.z;
+            if (pdf) pdf[k] = f.w;
+        }
     }
 }
 
+#ifndef VNDF_PHILOX_MINB
+#define VNDF_PHILOX_MINB 1
+#endif
+#ifndef VNDF_PHILOX_V
+#define VNDF_PHILOX_V 4
+#endif
+
 template <int METHOD, bool PDF, int V>
-__global__ void __launch_bounds__(256) philox_kernel(uint64_t seed, uint64_t first, int64_t n,
+__global__ void __launch_bounds__(256, VNDF_PHILOX_MINB) philox_kernel(uint64_t seed, uint64_t first, int64_t n,
                                                      float* __restrict__ hxp, float* __restrict__ hyp,
                                                      float* __restrict__ hzp, float* __restrict__ pdfp,
                                                      FixQueue fq) {
@@ -306,9 +331,7 @@ __global__ void __launch_bounds__(256) count_philox_kernel(uint64_t seed, uint64
         const int64_t i = start + r * stride;
         bool flag = false;
         if (i < n) {
-            uint4 X, Y;
-            philox_xy(seed, first + (uint64_t)i, X, Y);
-            const Inputs in = c4_inputs_fp32(X, Y);
+            const Inputs in = c4_inputs_fp32(philox_sample(seed, first + (uint64_t)i));
             Sample o;
             flag = cap_fp32<true>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o);
         }
@@ -496,7 +519,7 @@ vndf_status launch_philox_v(uint64_t seed, uint64_t first, int64_t n, float* hx,
         int sms = 0, dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        philox_fixup_kernel<<<std::max(sms, 1) * 4, 128, 0, s>>>(seed, first, fq, hx, hy, hz, pdf);
+        philox_fixup_kernel<<<std::max(sms, 1) * 4, 128, 0, s>>>(seed, first, n, fq, hx, hy, hz, pdf);
         e = cudaGetLastError();
     }
     if (qbuf) {
@@ -511,13 +534,14 @@ vndf_status launch_philox(uint64_t seed, uint64_t first, int64_t n, float* hx, f
                           float* pdf, cudaStream_t s) {
     vndf_status st = validate_philox_out(n, hx, hy, hz, pdf);
     if (st != VNDF_OK || n == 0) return st;
-    bool v4 = aligned(hx, 16) && aligned(hy, 16) && aligned(hz, 16) && (!pdf || aligned(pdf, 16));
+    constexpr int PV = VNDF_PHILOX_V;
+    bool v4 = aligned(hx, 4 * PV) && aligned(hy, 4 * PV) && aligned(hz, 4 * PV) && (!pdf || aligned(pdf, 4 * PV));
     if (prefs().vector_width == 1) v4 = false;
     if (pdf) {
-        return v4 ? launch_philox_v<METHOD, true, 4>(seed, first, n, hx, hy, hz, pdf, s)
+        return v4 ? launch_philox_v<METHOD, true, PV>(seed, first, n, hx, hy, hz, pdf, s)
                   : launch_philox_v<METHOD, true, 1>(seed, first, n, hx, hy, hz, pdf, s);
     }
-    return v4 ? launch_philox_v<METHOD, false, 4>(seed, first, n, hx, hy, hz, pdf, s)
+    return v4 ? launch_philox_v<METHOD, false, PV>(seed, first, n, hx, hy, hz, pdf, s)
               : launch_philox_v<METHOD, false, 1>(seed, first, n, hx, hy, hz, pdf, s);
 }
 

@@ -254,11 +254,12 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
     return c;
 }
 
-__device__ __forceinline__ double u01d(uint32_t w) {
-    return (double)(w >> 8) * 0x1p-24;
-}
-
-// Config-4 inputs from the two Philox blocks X, Y (vndf.h, DESIGN.md s.5).
+// Config-4 inputs from ONE Philox4x32-10 block per sample (counter = sample
+// index, key = seed; vndf.h, DESIGN.md s.5).  The 128 bits are split as
+//   u1 = W0[31:8] 2^-24, u2 = W1[31:8] 2^-24                 (the method's uniforms)
+//   ax = 0.01 * 100^(W2[31:8] 2^-24), ay = 0.01 * 100^(W3[31:8] 2^-24)
+//   ua = (W0[7:0] | W1[7:0] << 8) 2^-16, ub = (W2[7:0] | W3[7:0] << 8) 2^-16
+//   wi: z = 1 - ua, r = sqrt(ua (2 - ua)), phi = 2 pi ub   (uniform upper hemisphere)
 constexpr float kLog2_100F = 6.64385618977472436f;
 constexpr double kLog2_100D = 6.64385618977472436;
 
@@ -270,46 +271,51 @@ struct Inputs {
 
 // The 24-bit integer of a word, as float: u(w) = fw(w) 2^-24 exactly.
 __device__ __forceinline__ float fw(uint32_t w) { return __uint2float_rn(w >> 8); }
+// The 16-bit integer made of the low bytes of two words, as float.
+__device__ __forceinline__ float fw16(uint32_t lo, uint32_t hi) {
+    return __uint2float_rn(__byte_perm(lo, hi, 0x7740) & 0xFFFFu);
+}
 
-__device__ __forceinline__ Inputs c4_inputs_fp32(uint4 X, uint4 Y) {
+__device__ __forceinline__ uint4 philox_sample(uint64_t seed, uint64_t i) {
+    return philox4x32_10(make_uint4((uint32_t)i, (uint32_t)(i >> 32), 0u, 0u),
+                         make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+}
+
+__device__ __forceinline__ Inputs c4_inputs_fp32(uint4 W) {
     Inputs in;
-    const float fa = fw(X.x);
-    const float ua = fa * 0x1p-24f;
-    const float z = fmaf(fa, -0x1p-24f, 1.0f);          // 1 - u(X0), exact
-    const float r = sqrt_approx(ua * (1.0f + z));       // sqrt(u (2 - u))
+    const float fa = fw16(W.x, W.y);
+    const float ua = fa * 0x1p-16f;
+    const float z = fmaf(fa, -0x1p-16f, 1.0f);          // 1 - ua, exact
+    const float r = sqrt_approx(ua * (1.0f + z));       // sqrt(ua (2 - ua))
     float sp, cp;
-    sincos_2pi_reduced(fmaf(fw(X.y), 0x1p-24f, -0.5f), &sp, &cp);
+    sincos_2pi_reduced(fmaf(fw16(W.z, W.w), 0x1p-16f, -0.5f), &sp, &cp);
     in.wx = r * cp;
     in.wy = r * sp;
     in.wz = z;
     // 0.01 * 100^u = 2^((u - 1) log2 100); u log2 100 = fw (2^-24 log2 100) exactly
-    in.ax = ex2_approx(fmaf(fw(X.z), kLog2_100F * 0x1p-24f, -kLog2_100F));
-    in.ay = ex2_approx(fmaf(fw(X.w), kLog2_100F * 0x1p-24f, -kLog2_100F));
-    in.v1 = fmaf(fw(Y.x), 0x1p-24f, -0.5f);
-    const float f2 = fw(Y.y);
+    in.ax = ex2_approx(fmaf(fw(W.z), kLog2_100F * 0x1p-24f, -kLog2_100F));
+    in.ay = ex2_approx(fmaf(fw(W.w), kLog2_100F * 0x1p-24f, -kLog2_100F));
+    in.v1 = fmaf(fw(W.x), 0x1p-24f, -0.5f);
+    const float f2 = fw(W.y);
     in.u2 = f2 * 0x1p-24f;
     in.q = fmaf(f2, -0x1p-24f, 1.0f);
     return in;
 }
 
-__device__ __forceinline__ void philox_xy(uint64_t seed, uint64_t i, uint4& X, uint4& Y) {
-    const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
-    X = philox4x32_10(make_uint4((uint32_t)i, (uint32_t)(i >> 32), 0u, 0u), key);
-    Y = philox4x32_10(make_uint4((uint32_t)i, (uint32_t)(i >> 32), 1u, 0u), key);
-}
+__device__ __forceinline__ double u01d(uint32_t w) { return (double)(w >> 8) * 0x1p-24; }
 
-// Float64 fix-up for a config-4 sample: regenerate the words, build the inputs
+// Float64 fix-up for a config-4 sample: regenerate the word, build the inputs
 // in double from the exact uniforms, sample in double.
 __device__ __noinline__ float4 cap_philox_fp64(uint64_t seed, uint64_t i) {
-    uint4 X, Y;
-    philox_xy(seed, i, X, Y);
-    const double ua = u01d(X.x), ub = u01d(X.y);
+    const uint4 W = philox_sample(seed, i);
+    const double ua = (double)((W.x & 0xFFu) | ((W.y & 0xFFu) << 8)) * 0x1p-16;
+    const double ub = (double)((W.z & 0xFFu) | ((W.w & 0xFFu) << 8)) * 0x1p-16;
     const double r = sqrt(ua * (2.0 - ua));
     double sp, cp;
     sincospi(2.0 * ub, &sp, &cp);
-    const double ax = exp2((u01d(X.z) - 1.0) * kLog2_100D);
-    const double ay = exp2((u01d(X.w) - 1.0) * kLog2_100D);
-    return cap_fp64_d(r * cp, r * sp, 1.0 - ua, ax, ay, u01d(Y.x), u01d(Y.y));
+    const double ax = exp2((u01d(W.z) - 1.0) * kLog2_100D);
+    const double ay = exp2((u01d(W.w) - 1.0) * kLog2_100D);
+    return cap_fp64_d(r * cp, r * sp, 1.0 - ua, ax, ay, u01d(W.x), u01d(W.y));
 }
 
 }  // namespace vndf
