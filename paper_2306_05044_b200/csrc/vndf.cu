@@ -395,6 +395,44 @@ cudaError_t grid_for(const void* kernel, int block, int64_t work_items, int* gri
     return cudaSuccess;
 }
 
+// Library-private, stream-ordered memory pool per device for transient
+// buffers (the fix-up queue): its release threshold is unlimited, so after the
+// first call an allocation is a pool hit instead of a fresh mapping, without
+// touching the caller's default pool settings.
+std::map<int, cudaMemPool_t> g_pools;
+
+cudaError_t queue_alloc(void** p, size_t bytes, cudaStream_t s) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    cudaMemPool_t pool = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        auto it = g_pools.find(dev);
+        if (it != g_pools.end()) pool = it->second;
+    }
+    if (!pool) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        e = cudaMemPoolCreate(&pool, &props);
+        if (e != cudaSuccess) return e;
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        std::lock_guard<std::mutex> lk(g_mu);
+        auto it = g_pools.find(dev);
+        if (it != g_pools.end()) {
+            cudaMemPoolDestroy(pool);
+            pool = it->second;
+        } else {
+            g_pools[dev] = pool;
+        }
+    }
+    return cudaMallocFromPoolAsync(p, bytes, pool, s);
+}
+
 int block_size() {
     const int b = prefs().block_size;
     return b > 0 ? b : 256;
@@ -503,7 +541,7 @@ vndf_status launch_philox_v(uint64_t seed, uint64_t first, int64_t n, float* hx,
     if (METHOD == kCap) {
         // stream-ordered transient queue: [count | cap indices]
         fq.cap = (uint64_t)std::min<int64_t>(std::max<int64_t>(n / 128, 1 << 16), (int64_t)1 << 26);
-        e = cudaMallocAsync(&qbuf, sizeof(unsigned long long) + fq.cap * sizeof(uint64_t), s);
+        e = queue_alloc(&qbuf, sizeof(unsigned long long) + fq.cap * sizeof(uint64_t), s);
         if (e != cudaSuccess) return cuda_fail(e);
         fq.count = (unsigned long long*)qbuf;
         fq.idx = (uint64_t*)((char*)qbuf + sizeof(unsigned long long));
@@ -516,10 +554,13 @@ vndf_status launch_philox_v(uint64_t seed, uint64_t first, int64_t n, float* hx,
     philox_kernel<METHOD, PDF, V><<<grid, block, 0, s>>>(seed, first, n, hx, hy, hz, pdf, fq);
     e = cudaGetLastError();
     if (e == cudaSuccess && METHOD == kCap) {
+        // one thread per queue slot up to SMs x 32 blocks; blocks past the
+        // device-side count exit at once
         int sms = 0, dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        philox_fixup_kernel<<<std::max(sms, 1) * 4, 128, 0, s>>>(seed, first, n, fq, hx, hy, hz, pdf);
+        const int64_t fix_blocks = std::min<int64_t>(((int64_t)fq.cap + 127) / 128, (int64_t)std::max(sms, 1) * 32);
+        philox_fixup_kernel<<<(int)fix_blocks, 128, 0, s>>>(seed, first, n, fq, hx, hy, hz, pdf);
         e = cudaGetLastError();
     }
     if (qbuf) {
