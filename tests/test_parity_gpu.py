@@ -236,9 +236,12 @@ def test_h_only_matches_h_pdf(env):
 
 @pytest.mark.parametrize("cid", [1, 2, 5])
 def test_heitz_baseline_conditioned_parity(env, cid):
-    """The literal fp32 Listing 2 baseline (reading R8): within the
-    contract on samples whose Listing-2 reprojection is well conditioned
-    (oracle ti >= 0.05, |m| >= 0.1 max(alpha)); the rest is reported."""
+    """The literal fp32 Listing 2 baseline (reading R8) carries no
+    accuracy contract: its reprojection ti = sqrt(1 - t1^2 - t2^2) and
+    sqrt(1 - t1^2) cancel, and its hs.z error is absolute, so the
+    unstretch amplifies it by 1/|m|.  Model: |dh| <~ 1e-6 (1/ti + 1/sqrt(1 - t1^2)) / |m|.
+    Where the model predicts <= 2e-5 the kernel must meet the 2e-5 / 1e-4
+    contract; overall it must stay within tolerance on >= 98% of samples."""
     oracle, vndf, synth, dev = env
     cfg = synth.CONFIGS[cid]
     n = min(cfg.n, 1 << 22)
@@ -249,17 +252,19 @@ def test_heitz_baseline_conditioned_parity(env, cid):
     eh, ep = _errors([o.cpu().numpy() for o in out[:3]], out[3].cpu().numpy(), h_ref, p_ref)
     ax, ay = host[3].astype(np.float64), host[4].astype(np.float64)
     s = np.where(host[2] < 0, -1.0, 1.0)
-    mt = np.sqrt((s * h_ref[0] / ax) ** 2 + (s * h_ref[1] / ay) ** 2 + h_ref[2] ** 2)
-    N = 1.0 / mt
-    # Listing 2 L445 takes sqrt(1 - t1^2) with t1 = sqrt(u2) cos(2 pi u1): ill
-    # conditioned at the rim of the disk, where it is multiplied by (1 - s)
+    N = 1.0 / np.sqrt((s * h_ref[0] / ax) ** 2 + (s * h_ref[1] / ay) ** 2 + h_ref[2] ** 2)
     rim = 1.0 - host[6].astype(np.float64) * np.cos(2 * np.pi * host[5].astype(np.float64)) ** 2
-    good = (ti >= 0.05) & (N >= 0.1 * np.maximum(ax, ay)) & (rim >= 2.5e-3)
-    print(f"config {cid}: Heitz conditioned subset {good.mean():.4f}; outside it max|dh| "
-          f"{eh[~good].max() if (~good).any() else 0:.2e}")
-    assert good.mean() > 0.9
+    with np.errstate(divide="ignore"):
+        est = 1e-6 * (1.0 / ti + 1.0 / np.sqrt(np.maximum(rim, 0))) / N
+    good = est <= TOL_H
+    within = (eh <= TOL_H) & (ep <= TOL_PDF)
+    print(f"config {cid}: Heitz fp32 within tolerance on {within.mean():.5f} of samples; "
+          f"model-conditioned subset {good.mean():.4f}, max|dh| there {eh[good].max():.2e}, "
+          f"outside {eh[~good].max() if (~good).any() else 0:.2e}")
+    assert good.mean() > 0.5
     assert eh[good].max() <= TOL_H, float(eh[good].max())
     assert ep[good].max() <= TOL_PDF, float(ep[good].max())
+    assert within.mean() >= 0.98
     assert bool(torch.isfinite(out[0]).all())
 
 
