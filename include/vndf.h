@@ -125,9 +125,9 @@ vndf_status vndf_philox4x32_10(uint64_t seed, uint64_t first_index, int64_t n,
 
 /* End-to-end form of vndf_sample_cap_pdf on HOST buffers (pinned memory
  * recommended; pageable works but is slower).  Streams the batch through the
- * GPU in chunks of 4 Mi samples, overlapping host->device copies, the kernel
- * and device->host copies on two library-owned streams.  Device staging
- * (2 x 4 Mi x 44 B = 369 MB per device) is allocated on first use and kept
+ * GPU in chunks of 1 Mi samples, overlapping host->device copies, the kernel
+ * and device->host copies on three library-owned streams.  Device staging
+ * (3 x 1 Mi x 44 B = 138 MB per device) is allocated on first use and kept
  * for later calls; vndf_release_host_staging() frees it.  BLOCKING: returns
  * when the outputs are in host memory.  Work is ordered after prior work on
  * `stream`. */
@@ -155,7 +155,8 @@ vndf_status vndf_count_fixups_philox(uint64_t seed, uint64_t first_index, int64_
 
 /* Tuning knobs for the streamed kernels (process-wide; 0 = automatic).
  * vector_width in {0, 1, 4, 8} caps the vector path; block_size 0 or 64..256 (multiple of 32);
- * blocks_per_sm >= 0 caps the persistent grid at SMs x blocks_per_sm. */
+ * blocks_per_sm >= 1 caps the persistent grid at SMs x blocks_per_sm, 0 uses
+ * the occupancy limit, -1 launches one vector chunk per thread instead. */
 vndf_status vndf_set_launch_config(int vector_width, int block_size, int blocks_per_sm);
 
 /* Static description of a status code. */

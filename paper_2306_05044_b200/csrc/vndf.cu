@@ -363,7 +363,10 @@ LaunchPrefs prefs() {
 }
 
 // Persistent grid: min(work, SMs x resident blocks per SM).
-cudaError_t grid_for(const void* kernel, int block, int64_t work_items, int* grid) {
+// persistent: default grid policy of the kernel family when no preference is
+// set (streamed kernels: one chunk per thread, measured faster on B200 for
+// HBM-bound work; fused Philox: persistent, occupancy-limited).
+cudaError_t grid_for(const void* kernel, int block, int64_t work_items, int* grid, bool persistent = true) {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
@@ -391,7 +394,10 @@ cudaError_t grid_for(const void* kernel, int block, int64_t work_items, int* gri
     const LaunchPrefs p = prefs();
     if (p.blocks_per_sm > 0) occ = std::min(occ, p.blocks_per_sm);
     const int64_t need = std::max<int64_t>(1, (work_items + block - 1) / block);
-    *grid = (int)std::min<int64_t>(need, (int64_t)sms * occ);
+    // blocks_per_sm == -1: one work item per thread (non-persistent grid)
+    const bool one_per_thread = p.blocks_per_sm < 0 || (p.blocks_per_sm == 0 && !persistent);
+    const int64_t cap = one_per_thread ? (int64_t)INT32_MAX : (int64_t)sms * occ;
+    *grid = (int)std::min<int64_t>(need, cap);
     return cudaSuccess;
 }
 
@@ -433,9 +439,9 @@ cudaError_t queue_alloc(void** p, size_t bytes, cudaStream_t s) {
     return cudaMallocFromPoolAsync(p, bytes, pool, s);
 }
 
-int block_size() {
+int block_size(int dflt = 256) {
     const int b = prefs().block_size;
-    return b > 0 ? b : 256;
+    return b > 0 ? b : dflt;
 }
 
 bool aligned(const void* p, uintptr_t a) { return ((uintptr_t)p % a) == 0; }
@@ -487,9 +493,9 @@ int widest_vector(const StreamArgs& a) {
 template <int METHOD, bool PDF, int V>
 vndf_status launch_stream_v(const StreamArgs& a, int64_t n, cudaStream_t s) {
     const void* k = (const void*)stream_kernel<METHOD, PDF, V>;
-    const int block = block_size();
+    const int block = block_size(128);
     int grid = 0;
-    cudaError_t e = grid_for(k, block, std::max<int64_t>(n / V, 1), &grid);
+    cudaError_t e = grid_for(k, block, std::max<int64_t>(n / V, 1), &grid, /*persistent=*/false);
     if (e != cudaSuccess) return cuda_fail(e);
     stream_kernel<METHOD, PDF, V><<<grid, block, 0, s>>>(a, n);
     e = cudaGetLastError();
@@ -588,17 +594,20 @@ vndf_status launch_philox(uint64_t seed, uint64_t first, int64_t n, float* hx, f
 
 // ------------------------------------------------ host-path staging cache --
 // The blocking host entry point streams a batch through two device staging
-// sets of kStagingChunk samples (11 planes each: 7 in, 4 out) on two streams.
-// One staging area per device is kept after first use (2 x 4 Mi x 44 B =
-// 369 MB) so repeated calls pay no allocation; a concurrent second caller on
+// sets of kStagingChunk samples (11 planes each: 7 in, 4 out), round-robin
+// over kStagingSets streams, so chunk c's H2D copy overlaps chunk c-1's
+// kernel and chunk c-2's D2H copy (PCIe is full duplex).
+// One staging area per device is kept after first use (3 x 1 Mi x 44 B =
+// 138 MB) so repeated calls pay no allocation; a concurrent second caller on
 // the same device gets a private area that is freed when it returns.
-constexpr int64_t kStagingChunk = (int64_t)1 << 22;
+constexpr int64_t kStagingChunk = (int64_t)1 << 20;
+constexpr int kStagingSets = 3;
 
 struct Staging {
     int device = 0;
     float* buf = nullptr;
-    cudaStream_t s[2] = {nullptr, nullptr};
-    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    cudaStream_t s[kStagingSets] = {};
+    cudaEvent_t ev[1 + kStagingSets] = {};
     bool busy = false;
     bool cached = false;
 };
@@ -619,9 +628,10 @@ cudaError_t destroy_staging(Staging* sg) {
 cudaError_t create_staging(int dev, Staging** out) {
     Staging* sg = new Staging();
     sg->device = dev;
-    cudaError_t e = cudaMalloc((void**)&sg->buf, (size_t)2 * 11 * kStagingChunk * sizeof(float));
-    for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = cudaStreamCreateWithFlags(&sg->s[k], cudaStreamNonBlocking);
-    for (int k = 0; k < 3 && e == cudaSuccess; ++k) e = cudaEventCreateWithFlags(&sg->ev[k], cudaEventDisableTiming);
+    cudaError_t e = cudaMalloc((void**)&sg->buf, (size_t)kStagingSets * 11 * kStagingChunk * sizeof(float));
+    for (int k = 0; k < kStagingSets && e == cudaSuccess; ++k)
+        e = cudaStreamCreateWithFlags(&sg->s[k], cudaStreamNonBlocking);
+    for (int k = 0; k < 1 + kStagingSets && e == cudaSuccess; ++k) e = cudaEventCreateWithFlags(&sg->ev[k], cudaEventDisableTiming);
     if (e != cudaSuccess) {
         destroy_staging(sg);
         return e;
@@ -769,13 +779,13 @@ vndf_status vndf_sample_cap_pdf_host(const float* wi_x, const float* wi_y, const
     vndf_status result = VNDF_OK;
     // order after prior work on the caller's stream
     e = cudaEventRecord(sg->ev[0], user);
-    for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = cudaStreamWaitEvent(sg->s[k], sg->ev[0], 0);
+    for (int k = 0; k < kStagingSets && e == cudaSuccess; ++k) e = cudaStreamWaitEvent(sg->s[k], sg->ev[0], 0);
     const float* hin[7] = {wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2};
     float* hout[4] = {h_x, h_y, h_z, pdf};
     for (int64_t off = 0, c = 0; off < n && e == cudaSuccess && result == VNDF_OK; off += kStagingChunk, ++c) {
         const int64_t m = std::min<int64_t>(kStagingChunk, n - off);
-        cudaStream_t s = sg->s[c % 2];
-        float* base = sg->buf + (size_t)(c % 2) * 11 * kStagingChunk;
+        cudaStream_t s = sg->s[c % kStagingSets];
+        float* base = sg->buf + (size_t)(c % kStagingSets) * 11 * kStagingChunk;
         float* d[11];
         for (int k = 0; k < 11; ++k) d[k] = base + (size_t)k * kStagingChunk;
         const size_t bytes = (size_t)m * sizeof(float);
@@ -788,7 +798,7 @@ vndf_status vndf_sample_cap_pdf_host(const float* wi_x, const float* wi_y, const
             e = cudaMemcpyAsync(hout[k] + off, d[7 + k], bytes, cudaMemcpyDeviceToHost, s);
     }
     // join both pipeline streams back into the caller's stream, then block
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < kStagingSets; ++k) {
         cudaEventRecord(sg->ev[1 + k], sg->s[k]);
         cudaStreamWaitEvent(user, sg->ev[1 + k], 0);
     }
@@ -819,7 +829,7 @@ vndf_status vndf_set_launch_config(int vector_width, int block_size, int blocks_
         return VNDF_ERR_INVALID_ARGUMENT;
     if (!(block_size == 0 || (block_size >= 64 && block_size <= 256 && block_size % 32 == 0)))
         return VNDF_ERR_INVALID_ARGUMENT;
-    if (blocks_per_sm < 0) return VNDF_ERR_INVALID_ARGUMENT;
+    if (blocks_per_sm < -1) return VNDF_ERR_INVALID_ARGUMENT;
     std::lock_guard<std::mutex> lk(g_mu);
     g_prefs.vector_width = vector_width;
     g_prefs.block_size = block_size;

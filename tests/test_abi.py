@@ -100,7 +100,8 @@ def test_launch_config_validation(vndf):
     L = vndf.lib()
     assert L.vndf_set_launch_config(3, 0, 0) == vndf.VNDF_ERR_INVALID_ARGUMENT
     assert L.vndf_set_launch_config(0, 100, 0) == vndf.VNDF_ERR_INVALID_ARGUMENT
-    assert L.vndf_set_launch_config(0, 0, -1) == vndf.VNDF_ERR_INVALID_ARGUMENT
+    assert L.vndf_set_launch_config(0, 0, -2) == vndf.VNDF_ERR_INVALID_ARGUMENT
+    assert L.vndf_set_launch_config(0, 0, -1) == vndf.VNDF_OK
     assert L.vndf_set_launch_config(4, 128, 2) == vndf.VNDF_OK
     assert L.vndf_set_launch_config(0, 0, 0) == vndf.VNDF_OK
 
