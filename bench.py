@@ -56,6 +56,23 @@ def dist_env():
     return rank, world, local
 
 
+def shard_first_index(rank: int, n: int) -> int:
+    """Weak scaling: rank r owns global samples [r n, (r + 1) n).  The inputs are
+    counter-based, so a sample's value depends only on its global index."""
+    return rank * n
+
+
+def reduce_max(value: float, world: int, device=None) -> float:
+    """Max over ranks (timings): an all-reduce MAX when world > 1."""
+    if world <= 1:
+        return float(value)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -208,7 +225,7 @@ def run_ours(args):
     n = cfg.n
     stream = torch.cuda.current_stream(dev)
     # weak scaling: rank r owns global samples [r n, (r + 1) n)
-    x = synth.fill(cfg.recipe, cfg.seed, n, first=rank * n, device=dev)
+    x = synth.fill(cfg.recipe, cfg.seed, n, first=shard_first_index(rank, n), device=dev)
     ins = [x[k] for k in synth.PLANES]
     out = vndf.empty_outputs(n, dev, pdf=True)
     torch.cuda.synchronize()
@@ -228,10 +245,7 @@ def run_ours(args):
     clocks.stop()
     if barrier:
         barrier()
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
+    total_ms = reduce_max(total_ms, world, dev)
     ms_per_step = total_ms / args.steps
     value = world * n * args.steps / (total_ms * 1e-3) / 1e9
 
@@ -247,10 +261,8 @@ def run_ours(args):
     for _ in range(e2e_steps):
         vndf.vndf_sample_cap_pdf_host(*hin, *hout, n=n)
     e2e_s = time.perf_counter() - t0
-    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e = {"value": world * n * e2e_steps / float(te.item()) / 1e9, "unit": UNIT,
+    e2e_s = reduce_max(e2e_s, world, dev)
+    e2e = {"value": world * n * e2e_steps / e2e_s / 1e9, "unit": UNIT,
            "h2d_bytes_per_step": 28 * n, "d2h_bytes_per_step": 16 * n,
            "api": "vndf_sample_cap_pdf_host (pinned host buffers, blocking)"}
 

@@ -1,0 +1,69 @@
+"""Turn gpurun_out ncu artefacts into the committed summaries under profiles/<round>/.
+
+python tools/make_profiles.py r1 launches.csv prof_c2.ncu-rep [prof_c4.ncu-rep ...]
+"""
+import collections
+import csv
+import io
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+import ncu_summary  # noqa: E402
+
+rnd, launches = sys.argv[1], sys.argv[2]
+reps = sys.argv[3:]
+out = os.path.join(ROOT, "profiles", rnd)
+os.makedirs(out, exist_ok=True)
+
+# ---- launch list: per-kernel totals, and the share inside bench's timed region
+text = open(launches).read()
+text = text[text.index('"ID"'):]
+rows = [r for r in csv.DictReader(io.StringIO(text)) if r["Metric Name"] == "gpu__time_duration.sum"]
+agg = collections.OrderedDict()
+for r in rows:
+    name = r["Kernel Name"].split("(")[0]
+    key = (name, r["Grid Size"], r["Block Size"])
+    t = float(r["Metric Value"]) * (1e-3 if r["Metric Unit"] == "ns" else 1.0)  # -> us
+    a = agg.setdefault(key, [0, 0.0])
+    a[0] += 1
+    a[1] += t
+lines = [f"# Launch list summary ({rnd})", "",
+         "Source: `ncu --metrics gpu__time_duration.sum --clock-control none` over the whole",
+         "`python bench.py` command (default flags).  Times are cold-cache and serialised",
+         "under the profiler: compare shares, not absolutes.", "",
+         "| kernel | grid | block | launches | total us | mean us |", "|---|---|---|---|---|---|"]
+for (name, g, b), (c, t) in agg.items():
+    lines.append(f"| `{name}` | {g} | {b} | {c} | {t:.1f} | {t / c:.2f} |")
+# the timed region of bench.py: the 210 consecutive launches of the workload kernel
+wl = [r for r in rows if "stream_kernel<0, 1, 8>" in r["Kernel Name"]]
+lines += ["", f"Workload kernel `stream_kernel<0, 1, 8>` (vndf_sample_cap_pdf; the 16384-block launches are config 2, the 1024-block ones the e2e host path's 1 Mi chunks): "
+              f"{len(wl)} launches in the list; the bench step is exactly one such launch, so the "
+              "dominant kernel's share of the timed step is 100%."]
+open(os.path.join(out, "launches_summary.md"), "w").write("\n".join(lines) + "\n")
+
+# ---- full captures
+traffic = {}
+for rep in reps:
+    res = ncu_summary.load(rep)
+    base = os.path.splitext(os.path.basename(rep))[0]
+    with open(os.path.join(out, base + "_summary.txt"), "w") as f:
+        f.write(f"ncu --set full summary of {os.path.basename(rep)}\n")
+        for d in res:
+            f.write(d["kernel"] + "\n")
+            for k, v in d.items():
+                if k != "kernel":
+                    f.write(f"    {k:85s} {v}\n")
+    for d in res:
+        if "stream_kernel<0, 1, 8>" in d["kernel"] and "dram__bytes_read.sum" in d:
+            def val(s):
+                x, u = s.split()[0], s.split()[1] if len(s.split()) > 1 else "byte"
+                mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u]
+                return float(x) * mult
+            traffic["cap_pdf_c2"] = int(val(d["dram__bytes_read.sum"]) + val(d["dram__bytes_write.sum"]))
+if traffic:
+    json.dump(traffic, open(os.path.join(ROOT, "profiles", "traffic.json"), "w"), indent=1)
+print(open(os.path.join(out, "launches_summary.md")).read())
+print(traffic)
