@@ -345,11 +345,27 @@ def variants(torch, vndf, synth, dev, stream, x2, out2):
                               "t_heitz_over_t_cap": t_hz4 / t_cap4}
     del o4
     torch.cuda.empty_cache()
-    for v in res.values():
-        for k in list(v):
-            if isinstance(v[k], float):
-                v[k] = round(v[k], 4)
-    return res
+
+    # NEXT-1: sampler-only microbenchmark in the paper's methodology:
+    # 64 Listing-1 calls per lane, median of 100 dispatches
+    lanes, iters = 148 * 2048 * 4, 64
+    ck = torch.empty(lanes, dtype=torch.float32, device=dev)
+    mb = {}
+    for method, name in ((0, "cap"), (1, "heitz"), (2, "cap_literal")):
+        _, per = time_launches(torch, lambda: vndf.vndf_microbench(method, 5, lanes, iters, ck, stream=stream),
+                               100, 5, stream)
+        med = sorted(per)[len(per) // 2]
+        mb[name] = {"gsamples_s": lanes * iters / med / 1e6, "median_ms": med}
+    mb["t_heitz_over_t_cap"] = mb["heitz"]["median_ms"] / mb["cap"]["median_ms"]
+    mb["t_heitz_over_t_cap_literal"] = mb["heitz"]["median_ms"] / mb["cap_literal"]["median_ms"]
+    mb["paper"] = "t_Heitz/t_cap 1.3925 on RTX 2080, 1.5296 on Arc A770 (P:814-821)"
+    res["microbench_64_per_lane"] = mb
+    del ck
+    def rnd(v):
+        if isinstance(v, dict):
+            return {k: rnd(x) for k, x in v.items()}
+        return round(v, 4) if isinstance(v, float) else v
+    return rnd(res)
 
 
 def run_reference(args):

@@ -153,6 +153,21 @@ vndf_status vndf_count_fixups(const float *wi_x, const float *wi_y, const float 
 vndf_status vndf_count_fixups_philox(uint64_t seed, uint64_t first_index, int64_t n,
                                      uint64_t *count, vndf_stream_t stream);
 
+/* Sampler-only microbenchmark in the paper's GPU methodology (P:814-817:
+ * "calls Listing 1 64 times per lane").  Lane t (0 <= t < lanes) draws wi and
+ * (alpha_x, alpha_y) once from the config-4 recipe of index t (seed), then for
+ * k = 0 .. iters-1 samples h with u1 = u(W0 + k 0x9E3779B9), u2 = u(W1 + k
+ * 0x7F4A7C15) (32-bit wrap-around; W = that lane's Philox block), adds
+ * h.x + 2 h.y + 3 h.z to an fp32 checksum, and rotates wi about z:
+ * (x, y) <- (fma(c, x, -(s y)), fma(c, y, s x)) with c = 0.764842187f,
+ * s = 0.644217687f, every operation rounded to fp32 (so no call is
+ * loop-invariant).  checksum[t] is written once per lane.
+ * method: 0 = spherical cap (Listing 3, production fp32 arithmetic, no fix-up),
+ *         1 = Heitz 2018 (Listing 2), 2 = Listing 3 taken literally.
+ * No pdf.  checksum: device pointer to `lanes` floats. */
+vndf_status vndf_microbench(int method, uint64_t seed, int64_t lanes, int iters, float *checksum,
+                            vndf_stream_t stream);
+
 /* Tuning knobs for the streamed kernels (process-wide; 0 = automatic).
  * vector_width in {0, 1, 4, 8} caps the vector path; block_size 0 or 64..256 (multiple of 32);
  * blocks_per_sm >= 1 caps the persistent grid at SMs x blocks_per_sm, 0 uses

@@ -78,6 +78,7 @@ def lib() -> ctypes.CDLL:
         L.orc_batch_philox_words.argtypes = [u64, i64, P, u32, P]
         L.orc_batch_raycast.argtypes = [P, d, d, u64, i64, P, P, P]
         L.orc_batch_raycast.restype = u64
+        L.orc_batch_microbench.argtypes = [i32, u64, i64, i32, P]
         _lib = L
     return _lib
 
@@ -237,3 +238,10 @@ def batch_raycast(wi, ax, ay, seed: int, n: int):
     h = np.empty((3, n), dtype=np.float64)
     trials = lib().orc_batch_raycast(_p(_vec(wi)), ax, ay, seed, n, _p(h[0]), _p(h[1]), _p(h[2]))
     return h, trials
+
+
+def batch_microbench(method: int, seed: int, lanes: int, iters: int) -> np.ndarray:
+    """NEXT-1 microbenchmark checksums replayed in float64 (see oracle.c)."""
+    out = np.empty(lanes, dtype=np.float64)
+    lib().orc_batch_microbench(method, seed, lanes, iters, _p(out))
+    return out

@@ -340,6 +340,48 @@ void orc_c4_inputs(uint64_t seed, uint64_t index, double out[7])
 }
 
 /* ------------------------------------------------------------------------ */
+/* NEXT-1 sampler-only microbenchmark (the paper's GPU methodology: */
+/* Listing 1 called `iters` times per lane), replayed for lane t: inputs of  */
+/* the config-4 recipe of index t; iteration k: u1 = u(W0 + k A1), u2 =      */
+/* u(W1 + k A2) (32-bit wrap); h by the chosen listing in float64 from the   */
+/* CURRENT fp32 incidence; checksum += h.x + 2 h.y + 3 h.z; then the fp32    */
+/* rotation of (wi.x, wi.y) about z with single roundings (vndf.h):          */
+/* x' = fmaf(c, x, -(s*y)), y' = fmaf(c, y, s*x).  The incidence sequence is */
+/* fp32 by definition of the benchmark; the method arithmetic is float64.    */
+/* method: 0 = cap, 1 = Heitz, 2 = cap (Listing 3 literal: same math).       */
+/* ------------------------------------------------------------------------ */
+double orc_microbench_lane(int method, uint64_t seed, uint64_t lane, int iters)
+{
+    double in[7];
+    orc_c4_inputs(seed, lane, in);
+    uint32_t W[4];
+    orc_philox_block(seed, lane, 0u, W);
+    uint32_t x1 = W[0], x2 = W[1];
+    float wx = (float)in[0], wy = (float)in[1], wz = (float)in[2];
+    double ax = (double)(float)in[3], ay = (double)(float)in[4];
+    const float c = 0.764842187f, s = 0.644217687f;
+    double acc = 0.0;
+    for (int k = 0; k < iters; ++k) {
+        double wi[3] = {wx, wy, wz}, h[3];
+        orc_sample_vndf(method == 1 ? 1 : 0, wi, ax, ay, orc_u01(x1), orc_u01(x2), h, NULL);
+        acc += h[0] + 2.0 * h[1] + 3.0 * h[2];
+        x1 += 0x9E3779B9u;
+        x2 += 0x7F4A7C15u;
+        float sy = s * wy, sx = s * wx;
+        float rx = fmaf(c, wx, -sy);
+        float ry = fmaf(c, wy, sx);
+        wx = rx;
+        wy = ry;
+    }
+    return acc;
+}
+
+void orc_batch_microbench(int method, uint64_t seed, int64_t lanes, int iters, double *out)
+{
+    for (int64_t t = 0; t < lanes; ++t) out[t] = orc_microbench_lane(method, seed, (uint64_t)t, iters);
+}
+
+/* ------------------------------------------------------------------------ */
 /* Batched drivers (std::thread-like partition over contiguous ranges).     */
 /* ------------------------------------------------------------------------ */
 typedef struct {

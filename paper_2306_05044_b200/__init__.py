@@ -28,6 +28,7 @@ SYMBOLS = (
     "vndf_sample_cap_philox", "vndf_sample_heitz2018_philox", "vndf_philox4x32_10",
     "vndf_sample_cap_pdf_host", "vndf_release_host_staging", "vndf_count_fixups", "vndf_count_fixups_philox",
     "vndf_set_launch_config", "vndf_status_string", "vndf_last_cuda_error", "vndf_version",
+    "vndf_microbench",
 )
 
 
@@ -63,6 +64,7 @@ def lib() -> ctypes.CDLL:
         L.vndf_count_fixups_philox.argtypes = [u64, u64, i64, P, P]
         L.vndf_set_launch_config.argtypes = [i32, i32, i32]
         L.vndf_release_host_staging.argtypes = []
+        L.vndf_microbench.argtypes = [i32, u64, i64, i32, P, P]
         L.vndf_status_string.argtypes = [i32]
         L.vndf_status_string.restype = ctypes.c_char_p
         L.vndf_last_cuda_error.argtypes = []
@@ -236,6 +238,16 @@ def vndf_sample_cap_pdf_host(wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, h_x, h_
     else:
         st = _stream(stream, None)
     _check("vndf_sample_cap_pdf_host", lib().vndf_sample_cap_pdf_host(*ptrs, n, st))
+
+
+MICROBENCH_CAP, MICROBENCH_HEITZ, MICROBENCH_CAP_LITERAL = 0, 1, 2
+
+
+def vndf_microbench(method, seed, lanes, iters, checksum, stream=None):
+    """NEXT-1 sampler-only microbenchmark: per-lane checksums."""
+    p, dev = _dev_ptr(checksum, int(lanes), "checksum")
+    _check("vndf_microbench", lib().vndf_microbench(int(method), int(seed), int(lanes), int(iters), p,
+                                                    _stream(stream, dev)))
 
 
 def vndf_release_host_staging():

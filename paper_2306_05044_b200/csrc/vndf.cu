@@ -339,6 +339,54 @@ __global__ void __launch_bounds__(256) count_philox_kernel(uint64_t seed, uint64
     }
 }
 
+// ------------------------------------- NEXT-1: sampler-only microbenchmark --
+// The paper's GPU methodology: each lane calls Listing 1 `iters`
+// times.  Lane t draws its incidence and roughness once from the config-4
+// recipe (Philox block of index t).  Iteration k uses the integer Weyl
+// sequence u1 = u(s1 + k A1), u2 = u(s2 + k A2) (s1 = W0, s2 = W1) and then
+// rotates wi about z by a fixed angle with explicitly rounded fp32 operations
+// (so every call does the full Listing 1 -- nothing is loop-invariant -- and
+// the host oracle can replay the exact fp32 incidences).  h.x + 2 h.y + 3 h.z
+// is summed into a per-lane checksum (the sink).  No pdf, no flag, no fix-up.
+// VARIANT 0 = cap (production fp32 arithmetic), 1 = Heitz (Listing 2),
+// 2 = Listing 3 literal.
+constexpr uint32_t kWeyl1 = 0x9E3779B9u, kWeyl2 = 0x7F4A7C15u;
+constexpr float kRotC = 0.764842187f, kRotS = 0.644217687f;  // cos, sin of 0.7 rad (fp32)
+
+template <int VARIANT>
+__global__ void __launch_bounds__(256) microbench_kernel(uint64_t seed, int64_t lanes, int iters,
+                                                         float* __restrict__ checksum) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= lanes) return;
+    const uint4 W = philox_sample(seed, (uint64_t)t);
+    const Inputs in = c4_inputs_fp32(W);
+    uint32_t x1 = W.x, x2 = W.y;
+    float wx = in.wx, wy = in.wy;
+    float acc = 0.0f;
+#pragma unroll 4
+    for (int k = 0; k < iters; ++k) {
+        const float v1 = fmaf(fw(x1), 0x1p-24f, -0.5f);
+        const float f2 = fw(x2);
+        Sample o;
+        if (VARIANT == 0) {
+            cap_fp32<false, false>(wx, wy, in.wz, in.ax, in.ay, v1, f2 * 0x1p-24f,
+                                   fmaf(f2, -0x1p-24f, 1.0f), o);
+        } else if (VARIANT == 1) {
+            heitz_fp32<false, false>(wx, wy, in.wz, in.ax, in.ay, v1, f2 * 0x1p-24f, o);
+        } else {
+            cap_literal_fp32(wx, wy, in.wz, in.ax, in.ay, v1, f2 * 0x1p-24f, o);
+        }
+        acc += o.x + 2.0f * o.y + 3.0f * o.z;
+        x1 += kWeyl1;
+        x2 += kWeyl2;
+        const float rx = __fmaf_rn(kRotC, wx, -__fmul_rn(kRotS, wy));
+        const float ry = __fmaf_rn(kRotC, wy, __fmul_rn(kRotS, wx));
+        wx = rx;
+        wy = ry;
+    }
+    checksum[t] = acc;
+}
+
 // =============================================================== host side ==
 thread_local int g_last_cuda_error = 0;
 
@@ -822,6 +870,24 @@ vndf_status vndf_release_host_staging(void) {
     }
     g_staging.clear();
     return first == cudaSuccess ? VNDF_OK : cuda_fail(first);
+}
+
+vndf_status vndf_microbench(int method, uint64_t seed, int64_t lanes, int iters, float* checksum,
+                            vndf_stream_t stream) {
+    if (lanes < 0 || iters < 0 || !checksum || !aligned(checksum, 4) || method < 0 || method > 2)
+        return VNDF_ERR_INVALID_ARGUMENT;
+    if (lanes == 0) return VNDF_OK;
+    const int block = 256;
+    const int64_t grid = (lanes + block - 1) / block;
+    if (grid > INT32_MAX) return VNDF_ERR_INVALID_ARGUMENT;
+    cudaStream_t s = (cudaStream_t)stream;
+    switch (method) {
+        case 0: microbench_kernel<0><<<(int)grid, block, 0, s>>>(seed, lanes, iters, checksum); break;
+        case 1: microbench_kernel<1><<<(int)grid, block, 0, s>>>(seed, lanes, iters, checksum); break;
+        default: microbench_kernel<2><<<(int)grid, block, 0, s>>>(seed, lanes, iters, checksum); break;
+    }
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? VNDF_OK : cuda_fail(e);
 }
 
 vndf_status vndf_set_launch_config(int vector_width, int block_size, int blocks_per_sm) {

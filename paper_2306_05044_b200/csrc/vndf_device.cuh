@@ -185,6 +185,30 @@ __device__ __noinline__ void cap_fix_stream(const float* __restrict__ wx, const 
 }
 
 // ---------------------------------------------------------------------------
+// Listing 1 around Listing 3 taken LITERALLY in fp32:
+//   z = fma(1 - u.y, 1 + wi.z, -wi.z); sinTheta = sqrt(clamp(1 - z z, 0, 1)).
+// Used only by the sampler-only microbenchmark (NEXT-1) to compare the
+// paper's own fp32 code with Listing 2 in the paper's methodology; the
+// production kernels use cap_fp32 (same cost class, no cancellation).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cap_literal_fp32(float wx, float wy, float wz, float ax, float ay,
+                                                 float v1, float u2, Sample& o) {
+    const float tx = ax * wx, ty = ay * wy;
+    const float invL = rsqrt_approx(fmaf(tx, tx, fmaf(ty, ty, wz * wz)));
+    const float wsx = tx * invL, wsy = ty * invL, wsz = wz * invL;
+    float sp, cp;
+    sincos_2pi_reduced(v1, &sp, &cp);
+    const float z = fmaf(1.0f - u2, 1.0f + wsz, -wsz);
+    const float st = sqrt_approx(fminf(fmaxf(fmaf(-z, z, 1.0f), 0.0f), 1.0f));
+    const float hx = fmaf(st, cp, wsx), hy = fmaf(st, sp, wsy), hz = z + wsz;
+    const float mx = ax * hx, my = ay * hy;
+    const float invN = rsqrt_approx(fmaf(mx, mx, fmaf(my, my, hz * hz)));
+    o.x = mx * invN;
+    o.y = my * invN;
+    o.z = hz * invN;
+}
+
+// ---------------------------------------------------------------------------
 // Heitz-2018 baseline, fp32: Listing 1 around Listing 2 taken
 // literally, with the same SFU primitives as the cap kernel.
 // pdf: Eq. 1 for a unit std-space normal hs:

@@ -22,7 +22,7 @@ for f in funcs[1:]:
     # backward branches
     loops = []
     for addr, t in instrs:
-        m = re.search(r"BRA (?:`\(\.L_x_\d+\) )?0x([0-9a-f]+)", t)
+        m = re.search(r"BRA(?:\.U)? (?:!?U?P\d+, )?(?:`\(\.L_x_\d+\) )?0x([0-9a-f]+)", t)
         if m and int(m.group(1), 16) < addr:
             loops.append((int(m.group(1), 16), addr))
     if not loops:
