@@ -205,6 +205,22 @@ def roofline(bytes_per_launch: float, launch_ms: float, kernel_key: str):
             "algorithmic_bytes_per_launch": int(bytes_per_launch)}
 
 
+def issue_roofline(gsamples_s: float, key: str, sm_mhz: float = None):
+    """Instruction-issue bound of a compute-bound kernel (DESIGN.md s.6.4): each
+    of the 4 SMSPs of the 148 SMs issues one warp-instruction per clock, so the
+    bound is 592 x f_SM / (warp-instructions per sample, ncu-counted)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            ipc = json.load(f)[key]
+    except Exception:
+        return None
+    f = (sm_mhz or 1965.0) * 1e6
+    peak = 148 * 4 * f / ipc / 1e9
+    return {"bound": "alu", "achieved": round(gsamples_s, 2), "peak": round(peak, 2),
+            "unit": "Gsamples/s", "frac": round(gsamples_s / peak, 4),
+            "model": f"148 SMs x 4 SMSPs x 1 warp-inst/clk at {f / 1e6:.0f} MHz / {ipc} warp-inst per sample (ncu)"}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -340,7 +356,8 @@ def variants(torch, vndf, synth, dev, stream, x2, out2):
     t_cap4 = timed(lambda: vndf.vndf_sample_cap_philox(c4.seed, 0, c4.n, *o4, stream=stream))
     t_hz4 = timed(lambda: vndf.vndf_sample_heitz2018_philox(c4.seed, 0, c4.n, *o4, stream=stream))
     res["c4_cap_philox"] = {"gsamples_s": c4.n / t_cap4 / 1e6, "ms": t_cap4,
-                            "write_gb_s": 16 * c4.n / t_cap4 / 1e6}
+                            "write_gb_s": 16 * c4.n / t_cap4 / 1e6,
+                            "roofline": issue_roofline(c4.n / t_cap4 / 1e6, "cap_philox_c4_warp_inst_per_sample")}
     res["c4_heitz_philox"] = {"gsamples_s": c4.n / t_hz4 / 1e6, "ms": t_hz4,
                               "t_heitz_over_t_cap": t_hz4 / t_cap4}
     del o4
@@ -348,7 +365,7 @@ def variants(torch, vndf, synth, dev, stream, x2, out2):
 
     # NEXT-1: sampler-only microbenchmark in the paper's methodology:
     # 64 Listing-1 calls per lane, median of 100 dispatches
-    lanes, iters = 148 * 2048 * 4, 64
+    lanes, iters = 148 * 2048 * 16, 64
     ck = torch.empty(lanes, dtype=torch.float32, device=dev)
     mb = {}
     for method, name in ((0, "cap"), (1, "heitz"), (2, "cap_literal")):

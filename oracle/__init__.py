@@ -79,6 +79,17 @@ def lib() -> ctypes.CDLL:
         L.orc_batch_raycast.argtypes = [P, d, d, u64, i64, P, P, P]
         L.orc_batch_raycast.restype = u64
         L.orc_batch_microbench.argtypes = [i32, u64, i64, i32, P]
+        L.orc_G2.argtypes = [P, P, P, d, d]
+        L.orc_G2.restype = d
+        L.orc_brdf_cos.argtypes = [P, P, d, d]
+        L.orc_brdf_cos.restype = d
+        L.orc_pdf_reflect.argtypes = [P, P, d, d]
+        L.orc_pdf_reflect.restype = d
+        L.orc_sample_reflect.argtypes = [i32, P, d, d, d, d, P]
+        L.orc_batch_sample_reflect.argtypes = [i32, i64] + [P] * 7 + [P]
+        L.orc_furnace.argtypes = [i32, P, d, d, u64, u64, i64, P]
+        L.orc_batch_pdf_reflect.argtypes = [i64, P, d, d, P, P, P, P]
+        L.orc_batch_brdf_cos.argtypes = [i64, P, d, d, P, P, P, P]
         _lib = L
     return _lib
 
@@ -245,3 +256,72 @@ def batch_microbench(method: int, seed: int, lanes: int, iters: int) -> np.ndarr
     out = np.empty(lanes, dtype=np.float64)
     lib().orc_batch_microbench(method, seed, lanes, iters, _p(out))
     return out
+
+
+# ------------------------------------------------------------------ NEXT-2 ---
+def G2(wm, wi, wo, ax, ay) -> float:
+    return lib().orc_G2(_p(_vec(wm)), _p(_vec(wi)), _p(_vec(wo)), ax, ay)
+
+
+def brdf_cos(wi, wo, ax, ay) -> float:
+    """Eq. 11 x cos(theta_o) with F = 1."""
+    return lib().orc_brdf_cos(_p(_vec(wi)), _p(_vec(wo)), ax, ay)
+
+
+def pdf_reflect(wa, wb, ax, ay) -> float:
+    """Eq. 20."""
+    return lib().orc_pdf_reflect(_p(_vec(wa)), _p(_vec(wb)), ax, ay)
+
+
+def sample_reflect(method, wa, ax, ay, u1, u2) -> np.ndarray:
+    out = np.zeros(5)
+    lib().orc_sample_reflect(method, _p(_vec(wa)), ax, ay, u1, u2, _p(out))
+    return out
+
+
+def batch_sample_reflect(method, wx, wy, wz, ax, ay, u1, u2) -> np.ndarray:
+    """(5, n): wb.xyz, pdf (Eq. 20), weight (f_r cos / pdf)."""
+    planes = [np.ascontiguousarray(np.asarray(a, dtype=np.float32).reshape(-1))
+              for a in (wx, wy, wz, ax, ay, u1, u2)]
+    n = planes[0].size
+    out = np.empty((n, 5), dtype=np.float64)
+    lib().orc_batch_sample_reflect(method, n, *[_p(a) for a in planes], _p(out))
+    return out.T.copy()
+
+
+def furnace(method, wa, ax, ay, seed, n, first=0):
+    """Eq. 19 white-furnace estimator: (sum, sum of squares) of the weights."""
+    out = np.zeros(2)
+    lib().orc_furnace(method, _p(_vec(wa)), ax, ay, seed, first, n, _p(out))
+    return out
+
+
+def _batch_dirs(fn, wa, ax, ay, wb):
+    wb = np.ascontiguousarray(np.asarray(wb, dtype=np.float64).reshape(3, -1))
+    out = np.empty(wb.shape[1])
+    fn(wb.shape[1], _p(_vec(wa)), ax, ay, _p(wb[0]), _p(wb[1]), _p(wb[2]), _p(out))
+    return out
+
+
+def batch_pdf_reflect(wa, ax, ay, wb) -> np.ndarray:
+    return _batch_dirs(lib().orc_batch_pdf_reflect, wa, ax, ay, wb)
+
+
+def batch_brdf_cos(wa, ax, ay, wb) -> np.ndarray:
+    return _batch_dirs(lib().orc_batch_brdf_cos, wa, ax, ay, wb)
+
+
+def sphere_quadrature(nz: int = 512, nphi: int = 512, upper_only: bool = False):
+    """Directions and weights of a product rule on the sphere: Gauss-Legendre in
+    z = cos(theta) (uniform-area coordinate) times the midpoint rule in phi."""
+    x, w = np.polynomial.legendre.leggauss(nz)
+    if upper_only:
+        z, wz = 0.5 * (x + 1), 0.5 * w
+    else:
+        z, wz = x, w
+    phi = (np.arange(nphi) + 0.5) * (2 * np.pi / nphi)
+    Z, P = np.meshgrid(z, phi, indexing="ij")
+    r = np.sqrt(np.clip(1 - Z * Z, 0, None))
+    dirs = np.stack([r * np.cos(P), r * np.sin(P), Z]).reshape(3, -1)
+    weights = (wz[:, None] * np.full(nphi, 2 * np.pi / nphi)[None, :]).reshape(-1)
+    return dirs, weights

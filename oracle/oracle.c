@@ -340,6 +340,109 @@ void orc_c4_inputs(uint64_t seed, uint64_t index, double out[7])
 }
 
 /* ------------------------------------------------------------------------ */
+/* NEXT-2: BRDF importance sampling with the VNDF (appendix).  */
+/* Height-correlated Smith G2, Eq. 13-14:                       */
+/*   G2 = Gi Go / (Gi + Go - Gi Go), Gk = G1(wm, wk) (Eq. 15-17).            */
+/* ------------------------------------------------------------------------ */
+double orc_G2(const double wm[3], const double wi[3], const double wo[3], double ax, double ay)
+{
+    double gi = orc_G1(wm, wi, ax, ay), go = orc_G1(wm, wo, ax, ay);
+    double den = gi + go - gi * go;
+    return den > 0.0 ? gi * go / den : 0.0;
+}
+
+/* Eq. 11 times cos(theta_o), with F = 1 (the Fresnel term is not
+ * defined by the paper; reading in DESIGN.md s.3): for wi.z > 0,
+ *   f_r |cos theta_o| = G2(wh, wi, wo) D(wh) / (4 cos theta_i), wo.z > 0,
+ * 0 below the horizon (reflection only). wh = half vector (Eq. 6). */
+double orc_brdf_cos(const double wi[3], const double wo[3], double ax, double ay)
+{
+    if (!(wo[2] > 0.0) || !(wi[2] > 0.0)) return 0.0;
+    double wh[3];
+    orc_half_vector(wi, wo, wh);
+    return orc_G2(wh, wi, wo, ax, ay) * orc_D_ggx(wh, ax, ay) / (4.0 * wi[2]);
+}
+
+/* Eq. 20: PDF(wb, wa) = G1(wm, wa) D(wm) / (4 cos theta_a), with
+ * wm the half vector of (wa, wb), wa.z > 0. */
+double orc_pdf_reflect(const double wa[3], const double wb[3], double ax, double ay)
+{
+    double wm[3];
+    orc_half_vector(wa, wb, wm);
+    double d = wm[0] * wa[0] + wm[1] * wa[1] + wm[2] * wa[2];
+    if (!(d > 0.0)) return 0.0;
+    return orc_G1(wm, wa, ax, ay) * orc_D_ggx(wm, ax, ay) / (4.0 * wa[2]);
+}
+
+/* The appendix's two sampling steps, with reading R4 for
+ * wa.z < 0: (1) wm by Listing 1 (method 0 cap, 1 Heitz); (2) wb = reflect(wa,
+ * wm) (Eq. 5).  out = (wb.xyz, PDF Eq. 20, weight = f_r |cos theta_b| / PDF
+ * (= G2/G1 analytically)), evaluated in the upper frame s*wa. */
+void orc_sample_reflect(int method, const double wa_in[3], double ax, double ay, double u1,
+                        double u2, double out[5])
+{
+    double s = (wa_in[2] < 0.0) ? -1.0 : 1.0;
+    double n = sqrt(wa_in[0] * wa_in[0] + wa_in[1] * wa_in[1] + wa_in[2] * wa_in[2]);
+    double wa[3] = {s * wa_in[0] / n, s * wa_in[1] / n, s * wa_in[2] / n};
+    double wm[3], wb[3];
+    orc_sample_vndf(method, wa, ax, ay, u1, u2, wm, NULL);      /* step (1) */
+    orc_reflect(wa, wm, wb);                                    /* step (2), Eq. 5 */
+    double pdf = orc_pdf_reflect(wa, wb, ax, ay);               /* Eq. 20 */
+    out[0] = s * wb[0]; out[1] = s * wb[1]; out[2] = s * wb[2];
+    out[3] = pdf;
+    out[4] = pdf > 0.0 ? orc_brdf_cos(wa, wb, ax, ay) / pdf : 0.0;  /* Eq. 19 summand, L = 1 */
+}
+
+void orc_batch_sample_reflect(int method, int64_t n, const float *wx, const float *wy,
+                              const float *wz, const float *ax, const float *ay,
+                              const float *u1, const float *u2, double *out5)
+{
+    for (int64_t k = 0; k < n; ++k) {
+        double wa[3] = {wx[k], wy[k], wz[k]};
+        orc_sample_reflect(method, wa, ax[k], ay[k], u1[k], u2[k], out5 + 5 * k);
+    }
+}
+
+/* Fixed wa, alpha; arrays of wb (quadrature helpers for the pins). */
+void orc_batch_pdf_reflect(int64_t n, const double wa[3], double ax, double ay, const double *bx,
+                           const double *by, const double *bz, double *out)
+{
+    for (int64_t k = 0; k < n; ++k) {
+        double wb[3] = {bx[k], by[k], bz[k]};
+        out[k] = orc_pdf_reflect(wa, wb, ax, ay);
+    }
+}
+
+void orc_batch_brdf_cos(int64_t n, const double wa[3], double ax, double ay, const double *bx,
+                        const double *by, const double *bz, double *out)
+{
+    for (int64_t k = 0; k < n; ++k) {
+        double wb[3] = {bx[k], by[k], bz[k]};
+        out[k] = orc_brdf_cos(wa, wb, ax, ay);
+    }
+}
+
+/* White-furnace Monte Carlo estimator, Eq. 19 with L = 1:
+ * I = (1/N) sum_j f_r |cos| / PDF over N reflection samples of a fixed
+ * (wa, alpha); sample j uses u1 = u(W0), u2 = u(W1) of the Philox block
+ * (counter j, key seed).  Returns sum and sum of squares of the summands. */
+void orc_furnace(int method, const double wa[3], double ax, double ay, uint64_t seed,
+                 uint64_t first, int64_t n, double out2[2])
+{
+    double sum = 0.0, sq = 0.0;
+    for (int64_t j = 0; j < n; ++j) {
+        uint32_t W[4];
+        orc_philox_block(seed, first + (uint64_t)j, 0u, W);
+        double r[5];
+        orc_sample_reflect(method, wa, ax, ay, orc_u01(W[0]), orc_u01(W[1]), r);
+        sum += r[4];
+        sq += r[4] * r[4];
+    }
+    out2[0] = sum;
+    out2[1] = sq;
+}
+
+/* ------------------------------------------------------------------------ */
 /* NEXT-1 sampler-only microbenchmark (the paper's GPU methodology: */
 /* Listing 1 called `iters` times per lane), replayed for lane t: inputs of  */
 /* the config-4 recipe of index t; iteration k: u1 = u(W0 + k A1), u2 =      */

@@ -94,45 +94,110 @@ struct Sample {
 // v1 = u1 - 1/2 and q = 1 - u2 are passed precomputed (they are free when the
 // uniforms are generated in-kernel from integer words).  FLIP = false drops
 // the below-horizon handling for inputs known to have wi.z >= 0 (config 4).
-template <bool PDF, bool FLIP = true>
-__device__ __forceinline__ bool cap_fp32(float wx, float wy, float wz, float ax, float ay,
-                                         float v1, float u2, float q, Sample& o) {
-    const float s = (FLIP && wz < 0.0f) ? -1.0f : 1.0f;  // reading R4 (flip)
+// The shared body of the cap kernels: steps (1)-(3) up to the unnormalised
+// outputs, kept as named intermediates for the pdf / reflection epilogues.
+struct CapCore {
+    float s;              // flip sign (reading R4)
+    float L2;             // |M^-1 w|^2 of the (possibly non-unit) input w
+    float wz_u;           // s * w.z (upper-frame z of the input)
+    float a;              // 1 + ws.z
+    float hx, hy, hz;     // hs = c + ws (std space, unnormalised)
+    float mx, my;         // m = diag(ax, ay, 1) hs
+    float m2, invN;       // |m|^2, 1/|m|
+    float hs2;            // |hs|^2
+};
+
+template <bool FLIP>
+__device__ __forceinline__ CapCore cap_core(float wx, float wy, float wz, float ax, float ay, float v1,
+                                            float u2, float q) {
+    CapCore k;
+    k.s = (FLIP && wz < 0.0f) ? -1.0f : 1.0f;  // reading R4 (flip)
     // (1) warp to the hemisphere configuration: ws = M^-1 w / |M^-1 w|
     const float tx = ax * wx, ty = ay * wy;
-    const float L2 = fmaf(tx, tx, fmaf(ty, ty, wz * wz));
-    const float sinvL = s * rsqrt_approx(L2);
+    k.L2 = fmaf(tx, tx, fmaf(ty, ty, wz * wz));
+    const float sinvL = k.s * rsqrt_approx(k.L2);
     const float wsx = tx * sinvL, wsy = ty * sinvL, wsz = wz * sinvL;
+    k.wz_u = k.s * wz;
     // (2) sample the spherical cap z in (-ws.z, 1], phi = 2 pi u1
-    const float a = 1.0f + wsz;
-    const float hz = q * a;
+    k.a = 1.0f + wsz;
+    k.hz = q * k.a;
     const float rs2 = fmaf(wsx, wsx, wsy * wsy);
-    const float sin2 = u2 * fmaf(hz, a, rs2);
+    const float sin2 = u2 * fmaf(k.hz, k.a, rs2);
     const float st = sqrt_approx(sin2);
     float sp, cp;
     sincos_2pi_reduced(v1, &sp, &cp);
     // half vector hs = c + ws, not normalised
-    const float hx = fmaf(st, cp, wsx), hy = fmaf(st, sp, wsy);
-    // (3) warp back with M^-T = diag(ax, ay, 1) and normalise
-    const float mx = ax * hx, my = ay * hy;
-    const float m2 = fmaf(mx, mx, fmaf(my, my, hz * hz));
-    const float invN = rsqrt_approx(m2);
-    const float t = s * invN;
-    o.x = mx * t;
-    o.y = my * t;
-    o.z = hz * t;
-    const float hs2 = fmaf(hx, hx, fmaf(hy, hy, hz * hz));
-    if (PDF) {
-        const float num = m2 * (m2 * invN);                 // |m|^3
-        const float den = (kPiF * ax * ay) * a * hs2;
-        o.pdf = num * rcp_approx(den);
-    }
-    const float amax = fmaxf(ax, ay);
+    k.hx = fmaf(st, cp, wsx);
+    k.hy = fmaf(st, sp, wsy);
+    // (3) warp back with M^-T = diag(ax, ay, 1)
+    k.mx = ax * k.hx;
+    k.my = ay * k.hy;
+    k.m2 = fmaf(k.mx, k.mx, fmaf(k.my, k.my, k.hz * k.hz));
+    k.invN = rsqrt_approx(k.m2);
+    k.hs2 = fmaf(k.hx, k.hx, fmaf(k.hy, k.hy, k.hz * k.hz));
+    return k;
+}
+
+__device__ __forceinline__ bool cap_flag(const CapCore& k, float ax, float ay) {
 #ifdef VNDF_NO_FIXUP  // calibration builds only (tools/calibrate_flags.py)
     return false;
 #else
-    return (m2 < kFlagM * (amax * amax)) | (hs2 < kFlagHs);
+    const float amax = fmaxf(ax, ay);
+    return (k.m2 < kFlagM * (amax * amax)) | (k.hs2 < kFlagHs);
 #endif
+}
+
+template <bool PDF, bool FLIP = true>
+__device__ __forceinline__ bool cap_fp32(float wx, float wy, float wz, float ax, float ay,
+                                         float v1, float u2, float q, Sample& o) {
+    const CapCore k = cap_core<FLIP>(wx, wy, wz, ax, ay, v1, u2, q);
+    // normalise and flip back
+    const float t = k.s * k.invN;
+    o.x = k.mx * t;
+    o.y = k.my * t;
+    o.z = k.hz * t;
+    if (PDF) {
+        const float num = k.m2 * (k.m2 * k.invN);            // |m|^3
+        const float den = (kPiF * ax * ay) * k.a * k.hs2;
+        o.pdf = num * rcp_approx(den);
+    }
+    return cap_flag(k, ax, ay);
+}
+
+// ---------------------------------------------------------------------------
+// NEXT-2: reflection sampling (appendix steps (1)-(2)), its pdf
+// (Eq. 20) and the sample weight f_r cos / pdf = G2 / G1 (Eq. 11
+// with F = 1 and Eq. 13-17).  With unit w' = s w/|w|, L = |M^-1 w'|, z_i = w'.z:
+//   w'.h' = L |hs|^2 / (2 |m|)          (ws.hs = |hs|^2 / 2 on the cap)
+//   wo = 2 (w.h) h - w                  (Eq. 5)
+//   pdf_o = D_vis / (4 w.h) = |m|^4 / (2 pi ax ay (1 + ws.z) L |hs|^4)
+//   G2/G1 = z_o (z_i + L) / (L z_o + L_o z_i) if z_o > 0 else 0,
+//           L_o = |M^-1 wo'|            (height-correlated Smith, via Lambda)
+// ---------------------------------------------------------------------------
+struct Reflected {
+    float x, y, z, pdf, weight;
+};
+
+template <bool FLIP = true>
+__device__ __forceinline__ bool cap_reflect_fp32(float wx, float wy, float wz, float ax, float ay,
+                                                 float v1, float u2, float q, Reflected& o) {
+    const CapCore k = cap_core<FLIP>(wx, wy, wz, ax, ay, v1, u2, q);
+    const float inv_w = rsqrt_approx(fmaf(wx, wx, fmaf(wy, wy, wz * wz)));
+    const float L = k.L2 * rsqrt_approx(k.L2) * inv_w;       // |M^-1 w| / |w|
+    const float t = k.s * k.invN;
+    const float hx = k.mx * t, hy = k.my * t, hz = k.hz * t;  // h (output frame)
+    const float dot = 0.5f * L * k.hs2 * k.invN;              // w_unit . h >= 0
+    const float d2 = 2.0f * dot;
+    o.x = fmaf(d2, hx, -wx * inv_w);
+    o.y = fmaf(d2, hy, -wy * inv_w);
+    o.z = fmaf(d2, hz, -wz * inv_w);
+    const float m4 = k.m2 * k.m2, hs4 = k.hs2 * k.hs2;
+    o.pdf = m4 * rcp_approx((2.0f * kPiF * ax * ay) * k.a * L * hs4);
+    const float zi = k.wz_u * inv_w, zo = k.s * o.z;
+    const float Lo = sqrt_approx(fmaf(ax * o.x, ax * o.x, fmaf(ay * o.y, ay * o.y, o.z * o.z)));
+    const float wgt = zo * (zi + L) * rcp_approx(fmaf(L, zo, Lo * zi));
+    o.weight = zo > 0.0f ? wgt : 0.0f;
+    return cap_flag(k, ax, ay);
 }
 
 // ---------------------------------------------------------------------------
@@ -159,6 +224,49 @@ __device__ __forceinline__ float4 cap_fp64_d(double wx, double wy, double wz, do
     const double hs2 = hx * hx + hy * hy + hz * hz;
     const double pdf = m2 * N / (kPiD * ax * ay * a * hs2);
     return make_float4((float)(s * mx / N), (float)(s * my / N), (float)(s * hz / N), (float)pdf);
+}
+
+// Float64 reflection sample (fix-up of cap_reflect_fp32), same formulas.
+__device__ __forceinline__ void cap_reflect_fp64_d(double wx, double wy, double wz, double ax, double ay,
+                                                   double u1, double u2, double out[5]) {
+    const double s = (wz < 0.0) ? -1.0 : 1.0;
+    const double nw = sqrt(wx * wx + wy * wy + wz * wz);
+    const double ux = s * wx / nw, uy = s * wy / nw, uz = s * wz / nw;   // w'
+    const double tx = ax * ux, ty = ay * uy;
+    const double L = sqrt(tx * tx + ty * ty + uz * uz);
+    const double wsx = tx / L, wsy = ty / L, wsz = uz / L;
+    const double a = 1.0 + wsz, q = 1.0 - u2;
+    const double hz = q * a;
+    const double st = sqrt(u2 * (hz * a + wsx * wsx + wsy * wsy));
+    double sp, cp;
+    sincospi(2.0 * u1, &sp, &cp);
+    const double hx = st * cp + wsx, hy = st * sp + wsy;
+    const double mx = ax * hx, my = ay * hy;
+    const double m2 = mx * mx + my * my + hz * hz, N = sqrt(m2);
+    const double hs2 = hx * hx + hy * hy + hz * hz;
+    const double h0 = mx / N, h1 = my / N, h2 = hz / N;               // h' (upper frame)
+    const double dot = ux * h0 + uy * h1 + uz * h2;
+    const double ox = 2.0 * dot * h0 - ux, oy = 2.0 * dot * h1 - uy, oz = 2.0 * dot * h2 - uz;
+    const double Lo = sqrt(ax * ax * ox * ox + ay * ay * oy * oy + oz * oz);
+    out[0] = s * ox;
+    out[1] = s * oy;
+    out[2] = s * oz;
+    out[3] = m2 * m2 / (2.0 * kPiD * ax * ay * a * L * hs2 * hs2);
+    out[4] = oz > 0.0 ? oz * (uz + L) / (L * oz + Lo * uz) : 0.0;
+}
+
+__device__ __noinline__ void cap_reflect_fix_stream(const float* __restrict__ wx, const float* __restrict__ wy,
+                                                    const float* __restrict__ wz, const float* __restrict__ ax,
+                                                    const float* __restrict__ ay, const float* __restrict__ u1,
+                                                    const float* __restrict__ u2, float* ox, float* oy, float* oz,
+                                                    float* pdf, float* weight, int64_t i) {
+    double r[5];
+    cap_reflect_fp64_d(wx[i], wy[i], wz[i], ax[i], ay[i], u1[i], u2[i], r);
+    ox[i] = (float)r[0];
+    oy[i] = (float)r[1];
+    oz[i] = (float)r[2];
+    pdf[i] = (float)r[3];
+    weight[i] = (float)r[4];
 }
 
 // Out-of-line entry for the streamed kernels: widening happens in here, so the
