@@ -153,6 +153,32 @@ vndf_status vndf_count_fixups(const float *wi_x, const float *wi_y, const float 
 vndf_status vndf_count_fixups_philox(uint64_t seed, uint64_t first_index, int64_t n,
                                      uint64_t *count, vndf_stream_t stream);
 
+/* BRDF importance sampling with the VNDF, the appendix's two steps
+ * (P:1048-1055): (1) h by Listing 1 + Listing 3 (as vndf_sample_cap_pdf),
+ * (2) wo = reflect(w, h) = 2 (w.h) h - w with w = wi/|wi| (Eq. 5).  Outputs
+ * wo (3 planes), pdf = PDF(wo, w) of Eq. 20 = D_vis(h)/(4 w.h),
+ * and weight = f_r |cos theta_o| / pdf = G2/G1 (Eq. 11 with F = 1, Eq. 13-17;
+ * 0 when wo is below the horizon).  Below-horizon incidence: reading R4 (the
+ * reflection stays on the incident side).  28 B in, 20 B out per sample.
+ * Accuracy against the float64 oracle: |d wo| <= 6e-5 per component, pdf
+ * relative 1e-4, |d weight| <= 1e-4 (DESIGN.md s.6.5). */
+vndf_status vndf_sample_cap_reflect(const float *wi_x, const float *wi_y, const float *wi_z,
+                                    const float *alpha_x, const float *alpha_y,
+                                    const float *u1, const float *u2,
+                                    float *wo_x, float *wo_y, float *wo_z, float *pdf, float *weight,
+                                    int64_t n, vndf_stream_t stream);
+
+/* White-furnace Monte Carlo estimator, Eq. 19 with L = 1: for a
+ * fixed incidence wi and roughness, sample j = first_index .. first_index+n-1
+ * uses u1 = u(W0), u2 = u(W1) of the Philox block (counter j, key seed) and
+ * contributes its weight f_r |cos| / PDF.  Writes sums[0] = sum of weights,
+ * sums[1] = sum of squared weights (float64, DEVICE pointer); the estimate is
+ * sums[0]/n, its variance sums[1]/n - (sums[0]/n)^2.  method 0 = spherical cap,
+ * 1 = Heitz 2018.  Deterministic for a given device and n. */
+vndf_status vndf_furnace(int method, float wi_x, float wi_y, float wi_z, float alpha_x, float alpha_y,
+                         uint64_t seed, uint64_t first_index, int64_t n, double *sums,
+                         vndf_stream_t stream);
+
 /* Sampler-only microbenchmark in the paper's GPU methodology (P:814-817:
  * "calls Listing 1 64 times per lane").  Lane t (0 <= t < lanes) draws wi and
  * (alpha_x, alpha_y) once from the config-4 recipe of index t (seed), then for

@@ -28,7 +28,7 @@ SYMBOLS = (
     "vndf_sample_cap_philox", "vndf_sample_heitz2018_philox", "vndf_philox4x32_10",
     "vndf_sample_cap_pdf_host", "vndf_release_host_staging", "vndf_count_fixups", "vndf_count_fixups_philox",
     "vndf_set_launch_config", "vndf_status_string", "vndf_last_cuda_error", "vndf_version",
-    "vndf_microbench",
+    "vndf_microbench", "vndf_sample_cap_reflect", "vndf_furnace",
 )
 
 
@@ -65,6 +65,9 @@ def lib() -> ctypes.CDLL:
         L.vndf_set_launch_config.argtypes = [i32, i32, i32]
         L.vndf_release_host_staging.argtypes = []
         L.vndf_microbench.argtypes = [i32, u64, i64, i32, P, P]
+        L.vndf_sample_cap_reflect.argtypes = [P] * 12 + [i64, P]
+        f32 = ctypes.c_float
+        L.vndf_furnace.argtypes = [i32, f32, f32, f32, f32, f32, u64, u64, i64, P, P]
         L.vndf_status_string.argtypes = [i32]
         L.vndf_status_string.restype = ctypes.c_char_p
         L.vndf_last_cuda_error.argtypes = []
@@ -238,6 +241,24 @@ def vndf_sample_cap_pdf_host(wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, h_x, h_
     else:
         st = _stream(stream, None)
     _check("vndf_sample_cap_pdf_host", lib().vndf_sample_cap_pdf_host(*ptrs, n, st))
+
+
+def vndf_sample_cap_reflect(wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, wo_x, wo_y, wo_z, pdf, weight,
+                            n=None, stream=None):
+    """Appendix steps (1)-(2): reflected direction, Eq. 20 pdf, G2/G1 weight."""
+    n = _n(n, wi_x)
+    _stream_call("vndf_sample_cap_reflect",
+                 (wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, wo_x, wo_y, wo_z, pdf, weight),
+                 _IN + ("wo_x", "wo_y", "wo_z", "pdf", "weight"), n, stream)
+
+
+def vndf_furnace(method, wi, alpha, seed, n, sums, first_index=0, stream=None):
+    """Eq. 19 white-furnace estimator; sums: float64 CUDA tensor of 2 (sum, sum of squares)."""
+    import torch
+    p, dev = _dev_ptr(sums, 2, "sums", dtype=torch.float64)
+    _check("vndf_furnace", lib().vndf_furnace(int(method), float(wi[0]), float(wi[1]), float(wi[2]),
+                                              float(alpha[0]), float(alpha[1]), int(seed), int(first_index),
+                                              int(n), p, _stream(stream, dev)))
 
 
 MICROBENCH_CAP, MICROBENCH_HEITZ, MICROBENCH_CAP_LITERAL = 0, 1, 2

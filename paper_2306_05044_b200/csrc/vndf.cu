@@ -339,6 +339,142 @@ __global__ void __launch_bounds__(256) count_philox_kernel(uint64_t seed, uint64
     }
 }
 
+// ------------------------------------------ NEXT-2: reflection sampling --
+struct ReflectArgs {
+    const float* wx;
+    const float* wy;
+    const float* wz;
+    const float* ax;
+    const float* ay;
+    const float* u1;
+    const float* u2;
+    float* ox;
+    float* oy;
+    float* oz;
+    float* pdf;
+    float* weight;
+};
+
+// Streamed: 28 B in, 20 B out per sample (wo.xyz, pdf Eq. 20, weight G2/G1).
+template <int V>
+__global__ void __launch_bounds__(256) reflect_kernel(ReflectArgs a, int64_t n) {
+    const int64_t nchunks = n / V;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int64_t c = tid; c < nchunks; c += stride) {
+        const int64_t i = c * V;
+        const Vec<V> wx = ld_stream<V>(a.wx + i), wy = ld_stream<V>(a.wy + i),
+                     wz = ld_stream<V>(a.wz + i), ax = ld_stream<V>(a.ax + i),
+                     ay = ld_stream<V>(a.ay + i), u1 = ld_stream<V>(a.u1 + i),
+                     u2 = ld_stream<V>(a.u2 + i);
+        Vec<V> ox, oy, oz, pd, wt;
+        unsigned flags = 0;
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            Reflected r;
+            const bool f = cap_reflect_fp32(wx.v[j], wy.v[j], wz.v[j], ax.v[j], ay.v[j], u1.v[j] - 0.5f,
+                                            u2.v[j], 1.0f - u2.v[j], r);
+            flags |= (unsigned)f << j;
+            ox.v[j] = r.x;
+            oy.v[j] = r.y;
+            oz.v[j] = r.z;
+            pd.v[j] = r.pdf;
+            wt.v[j] = r.weight;
+        }
+        st_stream<V>(a.ox + i, ox);
+        st_stream<V>(a.oy + i, oy);
+        st_stream<V>(a.oz + i, oz);
+        st_stream<V>(a.pdf + i, pd);
+        st_stream<V>(a.weight + i, wt);
+        while (__builtin_expect(flags != 0, 0)) {
+            const int j = __ffs(flags) - 1;
+            flags &= flags - 1;
+            cap_reflect_fix_stream(a.wx, a.wy, a.wz, a.ax, a.ay, a.u1, a.u2, a.ox, a.oy, a.oz, a.pdf,
+                                   a.weight, i + j);
+        }
+    }
+    if (V > 1) {
+        const int64_t i = nchunks * V + tid;
+        if (i < n) {
+            Reflected r;
+            const float u2 = a.u2[i];
+            const bool f = cap_reflect_fp32(a.wx[i], a.wy[i], a.wz[i], a.ax[i], a.ay[i], a.u1[i] - 0.5f, u2,
+                                            1.0f - u2, r);
+            a.ox[i] = r.x;
+            a.oy[i] = r.y;
+            a.oz[i] = r.z;
+            a.pdf[i] = r.pdf;
+            a.weight[i] = r.weight;
+            if (f)
+                cap_reflect_fix_stream(a.wx, a.wy, a.wz, a.ax, a.ay, a.u1, a.u2, a.ox, a.oy, a.oz, a.pdf,
+                                       a.weight, i);
+        }
+    }
+}
+
+// White-furnace estimator, Eq. 19 with L = 1: for a fixed (wa, alpha), sample j
+// (u1 = u(W0), u2 = u(W1) of Philox block (counter j, key seed)) contributes
+// its weight f_r |cos| / PDF = G2/G1.  Per-thread float64 sums, fixed-order
+// block reduction, per-block partials; a one-block pass adds the partials in
+// block order (deterministic for a given grid).
+template <int METHOD>
+__global__ void __launch_bounds__(256) furnace_kernel(float wx, float wy, float wz, float ax, float ay,
+                                                      uint64_t seed, uint64_t first, int64_t n,
+                                                      double* __restrict__ partials) {
+    double s1 = 0.0, s2 = 0.0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
+        const uint4 W = philox_sample(seed, first + (uint64_t)j);
+        const float v1 = fmaf(fw(W.x), 0x1p-24f, -0.5f);
+        const float f2 = fw(W.y);
+        Reflected r;
+        if (METHOD == kCap) {
+            if (cap_reflect_fp32(wx, wy, wz, ax, ay, v1, f2 * 0x1p-24f, fmaf(f2, -0x1p-24f, 1.0f), r)) {
+                double d[5];
+                cap_reflect_fp64_d(wx, wy, wz, ax, ay, u01d(W.x), u01d(W.y), d);
+                r.weight = (float)d[4];
+            }
+        } else {
+            heitz_reflect_fp32(wx, wy, wz, ax, ay, v1, f2 * 0x1p-24f, r);
+        }
+        s1 += r.weight;
+        s2 += (double)r.weight * r.weight;
+    }
+    __shared__ double sh1[8], sh2[8];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s1 += __shfl_down_sync(0xffffffffu, s1, o);
+        s2 += __shfl_down_sync(0xffffffffu, s2, o);
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        sh1[warp] = s1;
+        sh2[warp] = s2;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a1 = 0.0, a2 = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            a1 += sh1[w];
+            a2 += sh2[w];
+        }
+        partials[2 * blockIdx.x] = a1;
+        partials[2 * blockIdx.x + 1] = a2;
+    }
+}
+
+__global__ void furnace_finish_kernel(const double* __restrict__ partials, int blocks, double* out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double a1 = 0.0, a2 = 0.0;
+        for (int b = 0; b < blocks; ++b) {
+            a1 += partials[2 * b];
+            a2 += partials[2 * b + 1];
+        }
+        out[0] = a1;
+        out[1] = a2;
+    }
+}
+
 // ------------------------------------- NEXT-1: sampler-only microbenchmark --
 // The paper's GPU methodology: each lane calls Listing 1 `iters`
 // times.  Lane t draws its incidence and roughness once from the config-4
@@ -870,6 +1006,84 @@ vndf_status vndf_release_host_staging(void) {
     }
     g_staging.clear();
     return first == cudaSuccess ? VNDF_OK : cuda_fail(first);
+}
+
+vndf_status vndf_sample_cap_reflect(const float* wi_x, const float* wi_y, const float* wi_z,
+                                    const float* alpha_x, const float* alpha_y, const float* u1,
+                                    const float* u2, float* wo_x, float* wo_y, float* wo_z, float* pdf,
+                                    float* weight, int64_t n, vndf_stream_t stream) {
+    if (n < 0) return VNDF_ERR_INVALID_ARGUMENT;
+    const void* in[7] = {wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2};
+    const void* out[5] = {wo_x, wo_y, wo_z, pdf, weight};
+    for (auto p : in)
+        if (!p || !aligned(p, 4)) return VNDF_ERR_INVALID_ARGUMENT;
+    for (auto p : out)
+        if (!p || !aligned(p, 4)) return VNDF_ERR_INVALID_ARGUMENT;
+    const int64_t bytes = n * (int64_t)sizeof(float);
+    for (int k = 0; k < 5; ++k) {
+        for (auto p : in)
+            if (n > 0 && overlaps(out[k], p, bytes)) return VNDF_ERR_INVALID_ARGUMENT;
+        for (int l = k + 1; l < 5; ++l)
+            if (n > 0 && overlaps(out[k], out[l], bytes)) return VNDF_ERR_INVALID_ARGUMENT;
+    }
+    if (n == 0) return VNDF_OK;
+    ReflectArgs a{wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, wo_x, wo_y, wo_z, pdf, weight};
+    int v = 8;
+    for (auto p : in) v = std::min(v, aligned(p, 32) ? 8 : aligned(p, 16) ? 4 : 1);
+    for (auto p : out) v = std::min(v, aligned(p, 32) ? 8 : aligned(p, 16) ? 4 : 1);
+    if (prefs().vector_width == 1) v = 1;
+    if (prefs().vector_width == 4) v = std::min(v, 4);
+    const int block = block_size(128);
+    int grid = 0;
+    cudaError_t e = cudaSuccess;
+    cudaStream_t s = (cudaStream_t)stream;
+    switch (v) {
+        case 8:
+            e = grid_for((const void*)reflect_kernel<8>, block, std::max<int64_t>(n / 8, 1), &grid, false);
+            if (e == cudaSuccess) reflect_kernel<8><<<grid, block, 0, s>>>(a, n);
+            break;
+        case 4:
+            e = grid_for((const void*)reflect_kernel<4>, block, std::max<int64_t>(n / 4, 1), &grid, false);
+            if (e == cudaSuccess) reflect_kernel<4><<<grid, block, 0, s>>>(a, n);
+            break;
+        default:
+            e = grid_for((const void*)reflect_kernel<1>, block, n, &grid, false);
+            if (e == cudaSuccess) reflect_kernel<1><<<grid, block, 0, s>>>(a, n);
+    }
+    if (e == cudaSuccess) e = cudaGetLastError();
+    return e == cudaSuccess ? VNDF_OK : cuda_fail(e);
+}
+
+vndf_status vndf_furnace(int method, float wi_x, float wi_y, float wi_z, float alpha_x, float alpha_y,
+                         uint64_t seed, uint64_t first_index, int64_t n, double* sums,
+                         vndf_stream_t stream) {
+    if (n < 0 || !sums || !aligned(sums, 8) || (method != 0 && method != 1)) return VNDF_ERR_INVALID_ARGUMENT;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (n == 0) {
+        const cudaError_t e = cudaMemsetAsync(sums, 0, 2 * sizeof(double), s);
+        return e == cudaSuccess ? VNDF_OK : cuda_fail(e);
+    }
+    const void* k = method == 0 ? (const void*)furnace_kernel<kCap> : (const void*)furnace_kernel<kHeitz>;
+    int grid = 0;
+    cudaError_t e = grid_for(k, 256, n, &grid, true);
+    if (e != cudaSuccess) return cuda_fail(e);
+    void* part = nullptr;
+    e = queue_alloc(&part, (size_t)grid * 2 * sizeof(double), s);
+    if (e != cudaSuccess) return cuda_fail(e);
+    if (method == 0)
+        furnace_kernel<kCap><<<grid, 256, 0, s>>>(wi_x, wi_y, wi_z, alpha_x, alpha_y, seed, first_index, n,
+                                                  (double*)part);
+    else
+        furnace_kernel<kHeitz><<<grid, 256, 0, s>>>(wi_x, wi_y, wi_z, alpha_x, alpha_y, seed, first_index,
+                                                    n, (double*)part);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) {
+        furnace_finish_kernel<<<1, 32, 0, s>>>((const double*)part, grid, sums);
+        e = cudaGetLastError();
+    }
+    const cudaError_t ef = cudaFreeAsync(part, s);
+    if (e == cudaSuccess) e = ef;
+    return e == cudaSuccess ? VNDF_OK : cuda_fail(e);
 }
 
 vndf_status vndf_microbench(int method, uint64_t seed, int64_t lanes, int iters, float* checksum,

@@ -370,6 +370,31 @@ __device__ __forceinline__ void heitz_fp32(float wx, float wy, float wz, float a
     }
 }
 
+// Heitz-2018 counterpart of cap_reflect_fp32 (same harness, for the furnace
+// comparison): h from Listing 2, then w.h directly, the general Eq. 20 form
+// pdf_h / (4 w.h) and the same G2/G1 weight.
+template <bool FLIP = true>
+__device__ __forceinline__ void heitz_reflect_fp32(float wx, float wy, float wz, float ax, float ay,
+                                                   float v1, float u2, Reflected& o) {
+    Sample h;
+    heitz_fp32<true, FLIP>(wx, wy, wz, ax, ay, v1, u2, h);
+    const float inv_w = rsqrt_approx(fmaf(wx, wx, fmaf(wy, wy, wz * wz)));
+    const float ux = wx * inv_w, uy = wy * inv_w, uz = wz * inv_w;
+    const float dot = fmaxf(fmaf(ux, h.x, fmaf(uy, h.y, uz * h.z)), 0.0f);
+    const float d2 = 2.0f * dot;
+    o.x = fmaf(d2, h.x, -ux);
+    o.y = fmaf(d2, h.y, -uy);
+    o.z = fmaf(d2, h.z, -uz);
+    o.pdf = h.pdf * rcp_approx(4.0f * dot);
+    const float s = (FLIP && wz < 0.0f) ? -1.0f : 1.0f;
+    const float zi = s * uz, zo = s * o.z;
+    const float L = sqrt_approx(fmaf(ax * ux, ax * ux, fmaf(ay * uy, ay * uy, uz * uz)));
+    const float Lo = sqrt_approx(fmaf(ax * o.x, ax * o.x, fmaf(ay * o.y, ay * o.y, o.z * o.z)));
+    const float wgt = zo * (zi + L) * rcp_approx(fmaf(L, zo, Lo * zi));
+    o.weight = zo > 0.0f ? wgt : 0.0f;
+}
+
+
 // ---------------------------------------------------------------------------
 // Philox4x32-10 (Salmon et al. SC'11), counter-based: no state, any index.
 // ---------------------------------------------------------------------------

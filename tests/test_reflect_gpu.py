@@ -1,0 +1,75 @@
+"""NEXT-2 on the GPU: reflection sampling (appendix steps (1)-(2))
+with the Eq. 20 pdf and the G2/G1 weight, and the Eq. 19 white-furnace
+estimator, against the float64 oracle.
+
+Tolerances (DESIGN.md s.6.5): wo <= 6e-5 per component (wo = 2(w.h)h - w moves
+by at most ~3x the h error), pdf relative 1e-4, weight absolute 1e-4."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL_WO, TOL_PDF, TOL_W = 6e-5, 1e-4, 1e-4
+
+
+@pytest.fixture(scope="module")
+def env():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+    __graft_entry__.build()
+    import oracle
+    import paper_2306_05044_b200 as vndf
+    import synth
+    return oracle, vndf, synth, torch.device("cuda:0")
+
+
+@pytest.mark.parametrize("cid,n", [(1, 1 << 16), (2, 1 << 22), (3, 1 << 21), (5, 1 << 22), (5, 4099)])
+def test_reflect_parity(env, cid, n):
+    oracle, vndf, synth, dev = env
+    cfg = synth.CONFIGS[cid]
+    x = synth.fill(cfg.recipe, cfg.seed, n, device=dev)
+    out = [torch.empty(n, dtype=torch.float32, device=dev) for _ in range(5)]
+    vndf.vndf_sample_cap_reflect(*[x[k] for k in synth.PLANES], *out)
+    torch.cuda.synchronize()
+    ref = oracle.batch_sample_reflect(oracle.CAP, *[x[k].cpu().numpy() for k in synth.PLANES])
+    got = np.stack([o.cpu().numpy() for o in out]).astype(np.float64)
+    ewo = np.abs(got[:3] - ref[:3]).max(axis=0)
+    epdf = np.abs(got[3] - ref[3]) / ref[3]
+    ew = np.abs(got[4] - ref[4])
+    print(f"config {cid}: max |dwo| {ewo.max():.2e}, pdf rel {epdf.max():.2e}, |dweight| {ew.max():.2e}")
+    assert ewo.max() <= TOL_WO, float(ewo.max())
+    assert epdf.max() <= TOL_PDF, float(epdf.max())
+    assert ew.max() <= TOL_W, float(ew.max())
+    # invariants: unit wo, mirror symmetry about h is implicit in the oracle; weights in [0, 1]
+    assert np.abs(np.linalg.norm(got[:3], axis=0) - 1).max() < 1e-5
+    assert got[4].min() >= 0.0 and got[4].max() <= 1.0 + 1e-6
+
+
+@pytest.mark.parametrize("method", [0, 1], ids=["cap", "heitz"])
+@pytest.mark.parametrize("theta,alpha", [(0, (0.1, 0.1)), (45, (0.5, 0.5)), (75, (0.3, 0.05)),
+                                         (85, (0.02, 0.02))])
+def test_furnace_gpu(env, method, theta, alpha):
+    """GPU Eq. 19 estimate equals the oracle's estimate on the same Philox
+    samples, and the quadrature albedo within 5 standard errors."""
+    oracle, vndf, synth, dev = env
+    t = np.radians(theta)
+    wa = np.array([np.sin(t) * np.cos(0.35), np.sin(t) * np.sin(0.35), np.cos(t)], dtype=np.float32)
+    n = 1 << 22
+    sums = torch.zeros(2, dtype=torch.float64, device=dev)
+    vndf.vndf_furnace(method, wa, alpha, 99, n, sums)
+    torch.cuda.synchronize()
+    s1, s2 = sums.cpu().numpy()
+    mean = s1 / n
+    var = s2 / n - mean * mean
+    m = 1 << 18
+    o1, _ = oracle.furnace(method, wa.astype(np.float64), *alpha, seed=99, n=m)
+    sums_m = torch.zeros(2, dtype=torch.float64, device=dev)
+    vndf.vndf_furnace(method, wa, alpha, 99, m, sums_m)
+    torch.cuda.synchronize()
+    assert abs(float(sums_m[0]) - o1) / m <= 1e-4  # per-sample weight tolerance
+    dirs, w = oracle.sphere_quadrature(nz=1024, nphi=1024, upper_only=True)
+    albedo = float((oracle.batch_brdf_cos(wa.astype(np.float64), *alpha, dirs) * w).sum())
+    se = np.sqrt(max(var, 0) / n)
+    assert abs(mean - albedo) <= 5 * se + 1e-5, (mean, albedo, se)
