@@ -49,7 +49,7 @@ def test_reflect_parity(env, cid, n):
 
 @pytest.mark.parametrize("method", [0, 1], ids=["cap", "heitz"])
 @pytest.mark.parametrize("theta,alpha", [(0, (0.1, 0.1)), (45, (0.5, 0.5)), (75, (0.3, 0.05)),
-                                         (85, (0.02, 0.02))])
+                                         (85, (0.2, 0.2)), (85, (0.02, 0.02))])
 def test_furnace_gpu(env, method, theta, alpha):
     """GPU Eq. 19 estimate equals the oracle's estimate on the same Philox
     samples, and the quadrature albedo within 5 standard errors."""
@@ -69,6 +69,10 @@ def test_furnace_gpu(env, method, theta, alpha):
     vndf.vndf_furnace(method, wa, alpha, 99, m, sums_m)
     torch.cuda.synchronize()
     assert abs(float(sums_m[0]) - o1) / m <= 1e-4  # per-sample weight tolerance
+    if alpha == (0.02, 0.02):
+        # at grazing incidence the reflected lobe is ~2 alpha cos(theta) = 3e-3 rad wide
+        # in azimuth: beyond the product quadrature; the oracle-equality check above holds
+        return
     dirs, w = oracle.sphere_quadrature(nz=1024, nphi=1024, upper_only=True)
     albedo = float((oracle.batch_brdf_cos(wa.astype(np.float64), *alpha, dirs) * w).sum())
     se = np.sqrt(max(var, 0) / n)
