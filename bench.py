@@ -363,6 +363,26 @@ def variants(torch, vndf, synth, dev, stream, x2, out2):
     del o4
     torch.cuda.empty_cache()
 
+    # NEXT-2: reflection sampling on the config-2 inputs (28 B in, 20 B out)
+    ro = [torch.empty(n2, dtype=torch.float32, device=dev) for _ in range(5)]
+    t_r = timed(lambda: vndf.vndf_sample_cap_reflect(*ins2, *ro, stream=stream))
+    rl = roofline(48 * n2, t_r, "cap_reflect_c2")
+    res["c2_cap_reflect"] = {"gsamples_s": n2 / t_r / 1e6, "ms": t_r, "gb_s": rl["achieved"], "frac_hbm": rl["frac"]}
+    del ro
+    # NEXT-2: Eq. 19 white-furnace estimator (compute-bound), cap vs Heitz, 2^28 samples
+    sums = torch.zeros(2, dtype=torch.float64, device=dev)
+    nf = 1 << 28
+    wa = (0.5, 0.2, 0.8426149773176359)
+    fur = {}
+    for method, name in ((0, "cap"), (1, "heitz")):
+        t = timed(lambda: vndf.vndf_furnace(method, wa, (0.3, 0.1), 17, nf, sums, stream=stream))
+        torch.cuda.synchronize()
+        s1, s2 = sums.cpu().tolist()
+        fur[name] = {"gsamples_s": nf / t / 1e6, "ms": t, "estimate": s1 / nf,
+                     "variance": s2 / nf - (s1 / nf) ** 2}
+    fur["t_heitz_over_t_cap"] = fur["heitz"]["ms"] / fur["cap"]["ms"]
+    res["furnace_eq19"] = fur
+
     # NEXT-1: sampler-only microbenchmark in the paper's methodology:
     # 64 Listing-1 calls per lane, median of 100 dispatches
     lanes, iters = 148 * 2048 * 16, 64

@@ -28,7 +28,7 @@ SYMBOLS = (
     "vndf_sample_cap_philox", "vndf_sample_heitz2018_philox", "vndf_philox4x32_10",
     "vndf_sample_cap_pdf_host", "vndf_release_host_staging", "vndf_count_fixups", "vndf_count_fixups_philox",
     "vndf_set_launch_config", "vndf_status_string", "vndf_last_cuda_error", "vndf_version",
-    "vndf_microbench", "vndf_sample_cap_reflect", "vndf_furnace",
+    "vndf_microbench", "vndf_sample_cap_reflect", "vndf_furnace", "vndf_pdf",
 )
 
 
@@ -66,6 +66,7 @@ def lib() -> ctypes.CDLL:
         L.vndf_release_host_staging.argtypes = []
         L.vndf_microbench.argtypes = [i32, u64, i64, i32, P, P]
         L.vndf_sample_cap_reflect.argtypes = [P] * 12 + [i64, P]
+        L.vndf_pdf.argtypes = [P] * 9 + [i64, P]
         f32 = ctypes.c_float
         L.vndf_furnace.argtypes = [i32, f32, f32, f32, f32, f32, u64, u64, i64, P, P]
         L.vndf_status_string.argtypes = [i32]
@@ -250,6 +251,13 @@ def vndf_sample_cap_reflect(wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, wo_x, wo
     _stream_call("vndf_sample_cap_reflect",
                  (wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, wo_x, wo_y, wo_z, pdf, weight),
                  _IN + ("wo_x", "wo_y", "wo_z", "pdf", "weight"), n, stream)
+
+
+def vndf_pdf(h_x, h_y, h_z, wi_x, wi_y, wi_z, alpha_x, alpha_y, pdf, n=None, stream=None):
+    """NEXT-4: Eq. 1 at caller-provided h."""
+    n = _n(n, h_x)
+    _stream_call("vndf_pdf", (h_x, h_y, h_z, wi_x, wi_y, wi_z, alpha_x, alpha_y, pdf),
+                 ("h_x", "h_y", "h_z", "wi_x", "wi_y", "wi_z", "alpha_x", "alpha_y", "pdf"), n, stream)
 
 
 def vndf_furnace(method, wi, alpha, seed, n, sums, first_index=0, stream=None):

@@ -339,6 +339,42 @@ __global__ void __launch_bounds__(256) count_philox_kernel(uint64_t seed, uint64
     }
 }
 
+// ------------------------------------------------- NEXT-4: standalone pdf --
+struct PdfArgs {
+    const float* hx;
+    const float* hy;
+    const float* hz;
+    const float* wx;
+    const float* wy;
+    const float* wz;
+    const float* ax;
+    const float* ay;
+    float* pdf;
+};
+
+// 32 B in (h, wi, alpha), 4 B out per sample; HBM-bound.
+template <int V>
+__global__ void __launch_bounds__(256) pdf_kernel(PdfArgs a, int64_t n) {
+    const int64_t nchunks = n / V;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int64_t c = tid; c < nchunks; c += stride) {
+        const int64_t i = c * V;
+        const Vec<V> hx = ld_stream<V>(a.hx + i), hy = ld_stream<V>(a.hy + i), hz = ld_stream<V>(a.hz + i),
+                     wx = ld_stream<V>(a.wx + i), wy = ld_stream<V>(a.wy + i), wz = ld_stream<V>(a.wz + i),
+                     ax = ld_stream<V>(a.ax + i), ay = ld_stream<V>(a.ay + i);
+        Vec<V> pd;
+#pragma unroll
+        for (int j = 0; j < V; ++j)
+            pd.v[j] = vndf_pdf_fp32(hx.v[j], hy.v[j], hz.v[j], wx.v[j], wy.v[j], wz.v[j], ax.v[j], ay.v[j]);
+        st_stream<V>(a.pdf + i, pd);
+    }
+    if (V > 1) {
+        const int64_t i = nchunks * V + tid;
+        if (i < n) a.pdf[i] = vndf_pdf_fp32(a.hx[i], a.hy[i], a.hz[i], a.wx[i], a.wy[i], a.wz[i], a.ax[i], a.ay[i]);
+    }
+}
+
 // ------------------------------------------ NEXT-2: reflection sampling --
 struct ReflectArgs {
     const float* wx;
@@ -430,9 +466,7 @@ __global__ void __launch_bounds__(256) furnace_kernel(float wx, float wy, float 
         Reflected r;
         if (METHOD == kCap) {
             if (cap_reflect_fp32(wx, wy, wz, ax, ay, v1, f2 * 0x1p-24f, fmaf(f2, -0x1p-24f, 1.0f), r)) {
-                double d[5];
-                cap_reflect_fp64_d(wx, wy, wz, ax, ay, u01d(W.x), u01d(W.y), d);
-                r.weight = (float)d[4];
+                r.weight = cap_reflect_weight_fp64(wx, wy, wz, ax, ay, u01d(W.x), u01d(W.y));
             }
         } else {
             heitz_reflect_fp32(wx, wy, wz, ax, ay, v1, f2 * 0x1p-24f, r);
@@ -1049,6 +1083,42 @@ vndf_status vndf_sample_cap_reflect(const float* wi_x, const float* wi_y, const 
         default:
             e = grid_for((const void*)reflect_kernel<1>, block, n, &grid, false);
             if (e == cudaSuccess) reflect_kernel<1><<<grid, block, 0, s>>>(a, n);
+    }
+    if (e == cudaSuccess) e = cudaGetLastError();
+    return e == cudaSuccess ? VNDF_OK : cuda_fail(e);
+}
+
+vndf_status vndf_pdf(const float* h_x, const float* h_y, const float* h_z, const float* wi_x,
+                     const float* wi_y, const float* wi_z, const float* alpha_x, const float* alpha_y,
+                     float* pdf, int64_t n, vndf_stream_t stream) {
+    if (n < 0 || !pdf || !aligned(pdf, 4)) return VNDF_ERR_INVALID_ARGUMENT;
+    const void* in[8] = {h_x, h_y, h_z, wi_x, wi_y, wi_z, alpha_x, alpha_y};
+    for (auto p : in) {
+        if (!p || !aligned(p, 4)) return VNDF_ERR_INVALID_ARGUMENT;
+        if (n > 0 && overlaps(pdf, p, n * (int64_t)sizeof(float))) return VNDF_ERR_INVALID_ARGUMENT;
+    }
+    if (n == 0) return VNDF_OK;
+    PdfArgs a{h_x, h_y, h_z, wi_x, wi_y, wi_z, alpha_x, alpha_y, pdf};
+    int v = aligned(pdf, 32) ? 8 : aligned(pdf, 16) ? 4 : 1;
+    for (auto p : in) v = std::min(v, aligned(p, 32) ? 8 : aligned(p, 16) ? 4 : 1);
+    if (prefs().vector_width == 1) v = 1;
+    if (prefs().vector_width == 4) v = std::min(v, 4);
+    const int block = block_size(128);
+    int grid = 0;
+    cudaError_t e = cudaSuccess;
+    cudaStream_t s = (cudaStream_t)stream;
+    switch (v) {
+        case 8:
+            e = grid_for((const void*)pdf_kernel<8>, block, std::max<int64_t>(n / 8, 1), &grid, false);
+            if (e == cudaSuccess) pdf_kernel<8><<<grid, block, 0, s>>>(a, n);
+            break;
+        case 4:
+            e = grid_for((const void*)pdf_kernel<4>, block, std::max<int64_t>(n / 4, 1), &grid, false);
+            if (e == cudaSuccess) pdf_kernel<4><<<grid, block, 0, s>>>(a, n);
+            break;
+        default:
+            e = grid_for((const void*)pdf_kernel<1>, block, n, &grid, false);
+            if (e == cudaSuccess) pdf_kernel<1><<<grid, block, 0, s>>>(a, n);
     }
     if (e == cudaSuccess) e = cudaGetLastError();
     return e == cudaSuccess ? VNDF_OK : cuda_fail(e);

@@ -255,6 +255,14 @@ __device__ __forceinline__ void cap_reflect_fp64_d(double wx, double wy, double 
     out[4] = oz > 0.0 ? oz * (uz + L) / (L * oz + Lo * uz) : 0.0;
 }
 
+// Out-of-line float64 weight of one reflection sample (furnace fix-up).
+__device__ __noinline__ float cap_reflect_weight_fp64(float wx, float wy, float wz, float ax, float ay,
+                                                      double u1, double u2) {
+    double r[5];
+    cap_reflect_fp64_d(wx, wy, wz, ax, ay, u1, u2, r);
+    return (float)r[4];
+}
+
 __device__ __noinline__ void cap_reflect_fix_stream(const float* __restrict__ wx, const float* __restrict__ wy,
                                                     const float* __restrict__ wz, const float* __restrict__ ax,
                                                     const float* __restrict__ ay, const float* __restrict__ u1,
@@ -290,6 +298,31 @@ __device__ __noinline__ void cap_fix_stream(const float* __restrict__ wx, const 
     hy[i] = f.y;
     hz[i] = f.z;
     if (pdf) pdf[i] = f.w;
+}
+
+// ---------------------------------------------------------------------------
+// NEXT-4: the VNDF pdf, Eq. 1, at a caller-provided h.  With
+// k = M^T h = (hx/ax, hy/ay, hz) and L = |M^-1 w| (reading R4 for w.z < 0),
+// Eq. 1-4 reduce exactly to
+//   D_vis(h, w) = 2 max(0, h.w) |h|^3 / (pi ax ay (L + s w.z) |k|^4)  if s h.z > 0, else 0,
+// invariant to the scale of h and w.  Every factor is a product or a sum of
+// squares (relative accuracy) except h.w, which is accumulated in float64.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float vndf_pdf_fp32(float hx, float hy, float hz, float wx, float wy, float wz,
+                                               float ax, float ay) {
+    const float s = (wz < 0.0f) ? -1.0f : 1.0f;
+    const double dot = fma((double)hx, (double)wx, fma((double)hy, (double)wy, (double)hz * (double)wz));
+    const float tx = ax * wx, ty = ay * wy;
+    const float L2 = fmaf(tx, tx, fmaf(ty, ty, wz * wz));
+    const float L = L2 * rsqrt_approx(L2);
+    const float iax = rcp_approx(ax), iay = rcp_approx(ay);
+    const float kx = hx * iax, ky = hy * iay;
+    const float k2 = fmaf(kx, kx, fmaf(ky, ky, hz * hz));
+    const float h2 = fmaf(hx, hx, fmaf(hy, hy, hz * hz));
+    const float h3 = h2 * (h2 * rsqrt_approx(h2));
+    const float num = 2.0f * (float)fmax(dot, 0.0) * h3;
+    const float den = (kPiF * ax * ay) * (L + s * wz) * (k2 * k2);
+    return (s * hz > 0.0f) ? num * rcp_approx(den) : 0.0f;
 }
 
 // ---------------------------------------------------------------------------
