@@ -89,6 +89,13 @@ def lib() -> ctypes.CDLL:
         L.orc_batch_sample_reflect.argtypes = [i32, i64] + [P] * 7 + [P]
         L.orc_furnace.argtypes = [i32, P, d, d, u64, u64, i64, P]
         L.orc_batch_pdf_reflect.argtypes = [i64, P, d, d, P, P, P, P]
+        L.orc_sample_vndf_native.argtypes = [i32, P, d, d, d, d, P]
+        L.orc_pdf_vndf_native.argtypes = [P, P, d, d]
+        L.orc_pdf_vndf_native.restype = d
+        L.orc_batch_raycast_native.argtypes = [P, d, d, u64, i64, P, P, P]
+        L.orc_batch_raycast_native.restype = u64
+        L.orc_batch_sample_native.argtypes = [i32, i64] + [P] * 7 + [P] * 4
+        L.orc_batch_pdf_native.argtypes = [i64, P, P, P, P, d, d, P]
         L.orc_batch_brdf_cos.argtypes = [i64, P, d, d, P, P, P, P]
         _lib = L
     return _lib
@@ -325,3 +332,38 @@ def sphere_quadrature(nz: int = 512, nphi: int = 512, upper_only: bool = False):
     dirs = np.stack([r * np.cos(P), r * np.sin(P), Z]).reshape(3, -1)
     weights = (wz[:, None] * np.full(nphi, 2 * np.pi / nphi)[None, :]).reshape(-1)
     return dirs, weights
+
+
+# ------------------------------------------------------------------ NEXT-3 ---
+def sample_vndf_native(method, wi, ax, ay, u1, u2) -> np.ndarray:
+    h = np.zeros(3)
+    lib().orc_sample_vndf_native(method, _p(_vec(wi)), ax, ay, u1, u2, _p(h))
+    return h
+
+
+def pdf_vndf_native(h, wi, ax, ay) -> float:
+    return lib().orc_pdf_vndf_native(_p(_vec(h)), _p(_vec(wi)), ax, ay)
+
+
+def batch_raycast_native(wi, ax, ay, seed: int, n: int):
+    h = np.empty((3, n), dtype=np.float64)
+    trials = lib().orc_batch_raycast_native(_p(_vec(wi)), ax, ay, seed, n, _p(h[0]), _p(h[1]), _p(h[2]))
+    return h, trials
+
+
+def batch_sample_native(method, wx, wy, wz, ax, ay, u1, u2, pdf=True):
+    planes = [np.ascontiguousarray(np.asarray(a, dtype=np.float32).reshape(-1))
+              for a in (wx, wy, wz, ax, ay, u1, u2)]
+    n = planes[0].size
+    h = np.empty((3, n), dtype=np.float64)
+    p = np.empty(n, dtype=np.float64) if pdf else None
+    lib().orc_batch_sample_native(method, n, *[_p(a) for a in planes], _p(h[0]), _p(h[1]), _p(h[2]),
+                                  _p(p) if pdf else None)
+    return h, p
+
+
+def batch_pdf_native(h, wi, ax, ay) -> np.ndarray:
+    h = np.ascontiguousarray(np.asarray(h, dtype=np.float64).reshape(3, -1))
+    out = np.empty(h.shape[1])
+    lib().orc_batch_pdf_native(h.shape[1], _p(h[0]), _p(h[1]), _p(h[2]), _p(_vec(wi)), ax, ay, _p(out))
+    return out

@@ -171,6 +171,21 @@ void orc_sample_vndf(int method, const double wi_in[3], double ax, double ay,
     h_out[0] = s * wm.x; h_out[1] = s * wm.y; h_out[2] = s * wm.z;
 }
 
+/* NEXT-3: the paper's NATIVE handling of incidence below the horizon (Fig. 4,
+ * theta_i = 130 deg): Listing 1 + Listing 3 (or 2) applied as
+ * printed to any wi with wi_std.z > -1 -- no flip.  The cap is (-ws.z, 1],
+ * which for ws.z < 0 lies above z = |ws.z|. */
+void orc_sample_vndf_native(int method, const double wi_in[3], double ax, double ay,
+                            double u1, double u2, double h_out[3])
+{
+    v3 wi = mk(wi_in[0], wi_in[1], wi_in[2]);
+    v3 wi_std = normalize(mk(wi.x * ax, wi.y * ay, wi.z));
+    v3 wm_std = method == 0 ? hemisphere_cap(u1, u2, wi_std)
+                            : hemisphere_heitz(u1, u2, wi_std, NULL);
+    v3 wm = normalize(mk(wm_std.x * ax, wm_std.y * ay, wm_std.z));
+    h_out[0] = wm.x; h_out[1] = wm.y; h_out[2] = wm.z;
+}
+
 /* ------------------------------------------------------------------------ */
 /* VNDF pdf, Eq. 1-4, written as defined.                      */
 /* ------------------------------------------------------------------------ */
@@ -205,6 +220,13 @@ double orc_pdf_vndf(const double h[3], const double wi[3], double ax, double ay)
     double s = (wi[2] < 0.0) ? -1.0 : 1.0;
     return vndf_pdf_upper(mk(s * h[0], s * h[1], s * h[2]),
                           mk(s * wi[0], s * wi[1], s * wi[2]), ax, ay);
+}
+
+/* Eq. 1 as defined for any wi (no flip): sigma_std(z_i) = (1 + z_i)/2 holds
+ * on [-1, 1] (Eq. 4) -- the native below-horizon pdf (NEXT-3). */
+double orc_pdf_vndf_native(const double h[3], const double wi[3], double ax, double ay)
+{
+    return vndf_pdf_upper(mk(h[0], h[1], h[2]), mk(wi[0], wi[1], wi[2]), ax, ay);
 }
 
 /* Eq. 12: GGX NDF D(wm) = D_std(M^T wm/|.|) |det M^T| / |M^T wm|^4 */
@@ -278,10 +300,10 @@ double orc_cap_density(const double wo[3], const double wi[3])
 /* Randomness: Philox block (trial, 2) of `seed` (independent of the u's).  */
 /* Returns the number of trials used.                                       */
 /* ------------------------------------------------------------------------ */
-uint64_t orc_sample_raycast(const double wi_in[3], double ax, double ay,
-                            uint64_t seed, uint64_t first_trial, double h_out[3])
+static uint64_t raycast(int flip, const double wi_in[3], double ax, double ay,
+                        uint64_t seed, uint64_t first_trial, double h_out[3])
 {
-    double s = (wi_in[2] < 0.0) ? -1.0 : 1.0;
+    double s = (flip && wi_in[2] < 0.0) ? -1.0 : 1.0;
     v3 wi = normalize(mk(s * wi_in[0], s * wi_in[1], s * wi_in[2]));
     /* orthonormal basis e1, e2 perpendicular to wi */
     v3 helper = fabs(wi.z) < 0.9 ? mk(0, 0, 1) : mk(1, 0, 0);
@@ -307,6 +329,49 @@ uint64_t orc_sample_raycast(const double wi_in[3], double ax, double ay,
         v3 n = normalize(mk(ax * ax * P.x, ay * ay * P.y, P.z));
         h_out[0] = s * n.x; h_out[1] = s * n.y; h_out[2] = s * n.z;
         return trial - first_trial + 1;
+    }
+}
+
+uint64_t orc_sample_raycast(const double wi_in[3], double ax, double ay,
+                            uint64_t seed, uint64_t first_trial, double h_out[3])
+{
+    return raycast(1, wi_in, ax, ay, seed, first_trial, h_out);
+}
+
+/* Native (no flip): rays travel along -wi even when wi points below the
+ * horizon; a ray counts if its first hit on the full ellipsoid is on the kept
+ * upper half (P:353-358 definition, NEXT-3). */
+uint64_t orc_batch_raycast_native(const double wi[3], double ax, double ay, uint64_t seed,
+                                  int64_t n, double *hx, double *hy, double *hz)
+{
+    uint64_t trial = 0;
+    for (int64_t k = 0; k < n; ++k) {
+        double h[3];
+        trial += raycast(0, wi, ax, ay, seed, trial, h);
+        hx[k] = h[0]; hy[k] = h[1]; hz[k] = h[2];
+    }
+    return trial;
+}
+
+void orc_batch_pdf_native(int64_t n, const double *hx, const double *hy, const double *hz,
+                          const double wi[3], double ax, double ay, double *out)
+{
+    for (int64_t k = 0; k < n; ++k) {
+        double h[3] = {hx[k], hy[k], hz[k]};
+        out[k] = orc_pdf_vndf_native(h, wi, ax, ay);
+    }
+}
+
+void orc_batch_sample_native(int method, int64_t n, const float *wx, const float *wy,
+                             const float *wz, const float *ax, const float *ay,
+                             const float *u1, const float *u2, double *hx, double *hy,
+                             double *hz, double *pdf)
+{
+    for (int64_t k = 0; k < n; ++k) {
+        double wi[3] = {wx[k], wy[k], wz[k]}, h[3];
+        orc_sample_vndf_native(method, wi, ax[k], ay[k], u1[k], u2[k], h);
+        hx[k] = h[0]; hy[k] = h[1]; hz[k] = h[2];
+        if (pdf) pdf[k] = orc_pdf_vndf_native(h, wi, ax[k], ay[k]);
     }
 }
 

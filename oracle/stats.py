@@ -12,14 +12,16 @@ from __future__ import annotations
 import numpy as np
 from scipy import stats as _st
 
-from . import batch_pdf
+from . import batch_pdf, batch_pdf_native
 
 NT = 64
 NP = 64
 
 
-def bin_masses(wi, ax: float, ay: float, nt: int = NT, npb: int = NP, q: int = 16) -> np.ndarray:
-    """Quadrature of pdf(h | wi) sin(theta) over each (theta, phi) bin."""
+def bin_masses(wi, ax: float, ay: float, nt: int = NT, npb: int = NP, q: int = 16,
+               native: bool = False) -> np.ndarray:
+    """Quadrature of pdf(h | wi) sin(theta) over each (theta, phi) bin (upper
+    hemisphere of h).  native=True evaluates Eq. 1 without the flip (NEXT-3)."""
     x, w = np.polynomial.legendre.leggauss(q)
     tb = np.linspace(0.0, np.pi / 2, nt + 1)
     pb = np.linspace(0.0, 2 * np.pi, npb + 1)
@@ -34,7 +36,10 @@ def bin_masses(wi, ax: float, ay: float, nt: int = NT, npb: int = NP, q: int = 1
     st = np.sin(TT)
     h = np.stack([st * np.cos(PP), st * np.sin(PP), np.cos(TT)]).reshape(3, -1)
     wi = np.asarray(wi, dtype=np.float64).reshape(3, 1)
-    f = batch_pdf(h, np.repeat(wi, h.shape[1], axis=1), ax, ay).reshape(TT.shape) * st
+    if native:
+        f = batch_pdf_native(h, wi[:, 0], ax, ay).reshape(TT.shape) * st
+    else:
+        f = batch_pdf(h, np.repeat(wi, h.shape[1], axis=1), ax, ay).reshape(TT.shape) * st
     f = f.reshape(nt, q, npb, q)
     m = np.einsum("aibj,i,j->ab", f, wt, wp)
     return m
