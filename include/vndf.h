@@ -91,6 +91,17 @@ vndf_status vndf_sample_cap_pdf(const float *wi_x, const float *wi_y, const floa
                                 float *h_x, float *h_y, float *h_z, float *pdf,
                                 int64_t n, vndf_stream_t stream);
 
+/* The paper's NATIVE handling of incidence below the horizon (NEXT-3; Fig. 4,
+ * theta_i = 130 deg): Listing 1 + Listing 3 applied as printed to
+ * any wi (no flip), the cap being (-ws.z, 1]; h is always an upper-hemisphere
+ * normal visible from wi, pdf = Eq. 1 with sigma_std = (1 + z_i)/2 (Eq. 4).
+ * Identical to vndf_sample_cap_pdf for wi.z >= 0.  pdf may be NULL. */
+vndf_status vndf_sample_cap_pdf_native(const float *wi_x, const float *wi_y, const float *wi_z,
+                                       const float *alpha_x, const float *alpha_y,
+                                       const float *u1, const float *u2,
+                                       float *h_x, float *h_y, float *h_z, float *pdf,
+                                       int64_t n, vndf_stream_t stream);
+
 /* Same-harness baseline: Listing 1 around Heitz's cross-section sampler,
  * Listing 2, literal fp32.  pdf may be NULL (h only). */
 vndf_status vndf_sample_heitz2018(const float *wi_x, const float *wi_y, const float *wi_z,

@@ -29,6 +29,7 @@ SYMBOLS = (
     "vndf_sample_cap_pdf_host", "vndf_release_host_staging", "vndf_count_fixups", "vndf_count_fixups_philox",
     "vndf_set_launch_config", "vndf_status_string", "vndf_last_cuda_error", "vndf_version",
     "vndf_microbench", "vndf_sample_cap_reflect", "vndf_furnace", "vndf_pdf",
+    "vndf_sample_cap_pdf_native",
 )
 
 
@@ -55,7 +56,8 @@ def lib() -> ctypes.CDLL:
                                   ctypes.c_uint32, ctypes.c_int)
         for name in ("vndf_sample_cap",):
             getattr(L, name).argtypes = [P] * 10 + [i64, P]
-        for name in ("vndf_sample_cap_pdf", "vndf_sample_heitz2018", "vndf_sample_cap_pdf_host"):
+        for name in ("vndf_sample_cap_pdf", "vndf_sample_heitz2018", "vndf_sample_cap_pdf_host",
+                     "vndf_sample_cap_pdf_native"):
             getattr(L, name).argtypes = [P] * 11 + [i64, P]
         for name in ("vndf_sample_cap_philox", "vndf_sample_heitz2018_philox"):
             getattr(L, name).argtypes = [u64, u64, i64, P, P, P, P, P]
@@ -155,6 +157,19 @@ def vndf_sample_cap_pdf(wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, h_x, h_y, h_
     _stream_call("vndf_sample_cap_pdf",
                  (wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, h_x, h_y, h_z, pdf),
                  _IN + ("h_x", "h_y", "h_z", "pdf"), n, stream)
+
+
+def vndf_sample_cap_pdf_native(wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, h_x, h_y, h_z, pdf=None,
+                               n=None, stream=None):
+    """NEXT-3: the paper's native below-horizon handling (Fig. 4), no flip."""
+    n = _n(n, wi_x)
+    dev = None
+    ptrs = []
+    for t, nm in zip((wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, h_x, h_y, h_z, pdf),
+                     _IN + ("h_x", "h_y", "h_z", "pdf")):
+        p, dev = _dev_ptr(t, n, nm, device=dev)
+        ptrs.append(p)
+    _check("vndf_sample_cap_pdf_native", lib().vndf_sample_cap_pdf_native(*ptrs, n, _stream(stream, dev)))
 
 
 def vndf_sample_heitz2018(wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, h_x, h_y, h_z, pdf=None,

@@ -30,7 +30,8 @@ using namespace vndf;
 
 namespace {
 
-enum Method { kCap = 0, kHeitz = 1 };
+// kCapNative: the paper's native below-horizon handling (NEXT-3, no flip)
+enum Method { kCap = 0, kHeitz = 1, kCapNative = 2 };
 
 struct StreamArgs {
     const float* wx;
@@ -118,12 +119,13 @@ __device__ __forceinline__ bool sample_one(float wx, float wy, float wz, float a
                                            float u2, Sample& o) {
     const float v1 = u1 - 0.5f;  // exact for u1 on the 2^-24 grid and for u1 >= 1/4
     if (METHOD == kCap) return cap_fp32<PDF>(wx, wy, wz, ax, ay, v1, u2, 1.0f - u2, o);
+    if (METHOD == kCapNative) return cap_fp32<PDF, false>(wx, wy, wz, ax, ay, v1, u2, 1.0f - u2, o);
     heitz_fp32<PDF>(wx, wy, wz, ax, ay, v1, u2, o);
     return false;
 }
 
-__device__ __forceinline__ void fix_one(const StreamArgs& a, bool pdf, int64_t i) {
-    cap_fix_stream(a.wx, a.wy, a.wz, a.ax, a.ay, a.u1, a.u2, a.hx, a.hy, a.hz, pdf ? a.pdf : nullptr, i);
+__device__ __forceinline__ void fix_one(const StreamArgs& a, bool pdf, int64_t i, bool flip) {
+    cap_fix_stream(a.wx, a.wy, a.wz, a.ax, a.ay, a.u1, a.u2, a.hx, a.hy, a.hz, pdf ? a.pdf : nullptr, i, flip);
 }
 
 // ------------------------------------------------------- streamed kernel --
@@ -160,11 +162,11 @@ __global__ void __launch_bounds__(256) stream_kernel(StreamArgs a, int64_t n) {
         st_stream<V>(a.hy + i, hy);
         st_stream<V>(a.hz + i, hz);
         if (PDF) st_stream<V>(a.pdf + i, pd);
-        if (METHOD == kCap && __builtin_expect(flags != 0, 0)) {
+        if (METHOD != kHeitz && __builtin_expect(flags != 0, 0)) {
             do {
                 const int j = __ffs(flags) - 1;
                 flags &= flags - 1;
-                fix_one(a, PDF, i + j);
+                fix_one(a, PDF, i + j, METHOD == kCap);
             } while (flags);
         }
     }
@@ -178,7 +180,7 @@ __global__ void __launch_bounds__(256) stream_kernel(StreamArgs a, int64_t n) {
             a.hy[i] = o.y;
             a.hz[i] = o.z;
             if (PDF) a.pdf[i] = o.pdf;
-            if (METHOD == kCap && f) fix_one(a, PDF, i);
+            if (METHOD != kHeitz && f) fix_one(a, PDF, i, METHOD == kCap);
         }
     }
 }
@@ -913,6 +915,17 @@ vndf_status vndf_sample_cap_pdf(const float* wi_x, const float* wi_y, const floa
     vndf_status st = validate_stream(a, true, n);
     if (st != VNDF_OK || n == 0) return st;
     return launch_stream<kCap, true>(a, n, (cudaStream_t)stream);
+}
+
+vndf_status vndf_sample_cap_pdf_native(const float* wi_x, const float* wi_y, const float* wi_z,
+                                       const float* alpha_x, const float* alpha_y, const float* u1,
+                                       const float* u2, float* h_x, float* h_y, float* h_z, float* pdf,
+                                       int64_t n, vndf_stream_t stream) {
+    const StreamArgs a = make_args(wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, h_x, h_y, h_z, pdf);
+    vndf_status st = validate_stream(a, false, n);
+    if (st != VNDF_OK || n == 0) return st;
+    return pdf ? launch_stream<kCapNative, true>(a, n, (cudaStream_t)stream)
+               : launch_stream<kCapNative, false>(a, n, (cudaStream_t)stream);
 }
 
 vndf_status vndf_sample_heitz2018(const float* wi_x, const float* wi_y, const float* wi_z,

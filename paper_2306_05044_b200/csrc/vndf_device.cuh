@@ -205,8 +205,8 @@ __device__ __forceinline__ bool cap_reflect_fp32(float wx, float wy, float wz, f
 // cap_fp32, IEEE double throughout (sincospi, sqrt, division).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ float4 cap_fp64_d(double wx, double wy, double wz, double ax, double ay,
-                                             double u1, double u2) {
-    const double s = (wz < 0.0) ? -1.0 : 1.0;
+                                             double u1, double u2, bool flip = true) {
+    const double s = (flip && wz < 0.0) ? -1.0 : 1.0;
     const double tx = ax * wx, ty = ay * wy;
     const double L = sqrt(tx * tx + ty * ty + wz * wz);
     const double wsx = s * tx / L, wsy = s * ty / L, wsz = s * wz / L;
@@ -292,8 +292,8 @@ __device__ __noinline__ void cap_fix_stream(const float* __restrict__ wx, const 
                                             const float* __restrict__ wz, const float* __restrict__ ax,
                                             const float* __restrict__ ay, const float* __restrict__ u1,
                                             const float* __restrict__ u2, float* hx, float* hy,
-                                            float* hz, float* pdf, int64_t i) {
-    const float4 f = cap_fp64_d(wx[i], wy[i], wz[i], ax[i], ay[i], u1[i], u2[i]);
+                                            float* hz, float* pdf, int64_t i, bool flip) {
+    const float4 f = cap_fp64_d(wx[i], wy[i], wz[i], ax[i], ay[i], u1[i], u2[i], flip);
     hx[i] = f.x;
     hy[i] = f.y;
     hz[i] = f.z;
