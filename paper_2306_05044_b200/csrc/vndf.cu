@@ -119,7 +119,7 @@ __device__ __forceinline__ bool sample_one(float wx, float wy, float wz, float a
                                            float u2, Sample& o) {
     const float v1 = u1 - 0.5f;  // exact for u1 on the 2^-24 grid and for u1 >= 1/4
     if (METHOD == kCap) return cap_fp32<PDF>(wx, wy, wz, ax, ay, v1, u2, 1.0f - u2, o);
-    if (METHOD == kCapNative) return cap_fp32<PDF, false>(wx, wy, wz, ax, ay, v1, u2, 1.0f - u2, o);
+    if (METHOD == kCapNative) return cap_fp32<PDF, kFrameNative>(wx, wy, wz, ax, ay, v1, u2, 1.0f - u2, o);
     heitz_fp32<PDF>(wx, wy, wz, ax, ay, v1, u2, o);
     return false;
 }
@@ -205,7 +205,7 @@ __device__ __forceinline__ Sample philox_one(uint64_t seed, uint64_t first, uint
     Sample o;
     if (METHOD == kCap) {
         // config-4 inputs are on the upper hemisphere (wi.z = 1 - u > 0): no flip
-        const bool flag = cap_fp32<PDF, false>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o);
+        const bool flag = cap_fp32<PDF, kFrameUpper>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o);
         if (__builtin_expect(flag, 0)) {
             const unsigned long long slot = atomicAdd(fq.count, 1ull);
             if (slot < fq.cap) fq.idx[slot] = k;
@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(128) philox_fixup_kernel(uint64_t seed, uint64
     for (uint64_t k = t0; k < (uint64_t)n; k += stride) {  // overflow: rescan
         const Inputs in = c4_inputs_fp32(philox_sample(seed, first + k));
         Sample o;
-        if (cap_fp32<true, false>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o)) {
+        if (cap_fp32<true, kFrameUpper>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o)) {
             const float4 f = cap_philox_fp64(seed, first + k);
             hx[k] = f.x;
             hy[k] = f.y;
@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(256) microbench_kernel(uint64_t seed, int64_t 
         const float f2 = fw(x2);
         Sample o;
         if (VARIANT == 0) {
-            cap_fp32<false, false>(wx, wy, in.wz, in.ax, in.ay, v1, f2 * 0x1p-24f,
+            cap_fp32<false, kFrameUpper>(wx, wy, in.wz, in.ax, in.ay, v1, f2 * 0x1p-24f,
                                    fmaf(f2, -0x1p-24f, 1.0f), o);
         } else if (VARIANT == 1) {
             heitz_fp32<false, false>(wx, wy, in.wz, in.ax, in.ay, v1, f2 * 0x1p-24f, o);

@@ -92,8 +92,8 @@ struct Sample {
 //   m = diag(ax, ay, 1) hs (the unnormalised output).
 // ---------------------------------------------------------------------------
 // v1 = u1 - 1/2 and q = 1 - u2 are passed precomputed (they are free when the
-// uniforms are generated in-kernel from integer words).  FLIP = false drops
-// the below-horizon handling for inputs known to have wi.z >= 0 (config 4).
+// uniforms are generated in-kernel from integer words).  FRAME selects the
+// handling of the incidence frame (kFrameFlip / kFrameUpper / kFrameNative).
 // The shared body of the cap kernels: steps (1)-(3) up to the unnormalised
 // outputs, kept as named intermediates for the pdf / reflection epilogues.
 struct CapCore {
@@ -107,11 +107,16 @@ struct CapCore {
     float hs2;            // |hs|^2
 };
 
-template <bool FLIP>
+// Frames of the incidence: kFrameFlip = reading R4 (wi.z < 0 is flipped);
+// kFrameUpper = inputs known to have wi.z >= 0 (config 4); kFrameNative = the
+// paper's native below-horizon handling (NEXT-3), where ws.z may be negative.
+constexpr int kFrameFlip = 0, kFrameUpper = 1, kFrameNative = 2;
+
+template <int FRAME>
 __device__ __forceinline__ CapCore cap_core(float wx, float wy, float wz, float ax, float ay, float v1,
                                             float u2, float q) {
     CapCore k;
-    k.s = (FLIP && wz < 0.0f) ? -1.0f : 1.0f;  // reading R4 (flip)
+    k.s = (FRAME == kFrameFlip && wz < 0.0f) ? -1.0f : 1.0f;  // reading R4 (flip)
     // (1) warp to the hemisphere configuration: ws = M^-1 w / |M^-1 w|
     const float tx = ax * wx, ty = ay * wy;
     k.L2 = fmaf(tx, tx, fmaf(ty, ty, wz * wz));
@@ -119,9 +124,11 @@ __device__ __forceinline__ CapCore cap_core(float wx, float wy, float wz, float 
     const float wsx = tx * sinvL, wsy = ty * sinvL, wsz = wz * sinvL;
     k.wz_u = k.s * wz;
     // (2) sample the spherical cap z in (-ws.z, 1], phi = 2 pi u1
-    k.a = 1.0f + wsz;
-    k.hz = q * k.a;
     const float rs2 = fmaf(wsx, wsx, wsy * wsy);
+    // a = 1 + ws.z; for ws.z < 0 (native frame only) 1 + ws.z cancels, use the
+    // identity 1 + ws.z = (1 - ws.z^2) / (1 - ws.z) = rs^2 / (1 - ws.z)
+    k.a = (FRAME == kFrameNative && wsz < 0.0f) ? rs2 * rcp_approx(1.0f - wsz) : 1.0f + wsz;
+    k.hz = q * k.a;
     const float sin2 = u2 * fmaf(k.hz, k.a, rs2);
     const float st = sqrt_approx(sin2);
     float sp, cp;
@@ -147,10 +154,10 @@ __device__ __forceinline__ bool cap_flag(const CapCore& k, float ax, float ay) {
 #endif
 }
 
-template <bool PDF, bool FLIP = true>
+template <bool PDF, int FRAME = kFrameFlip>
 __device__ __forceinline__ bool cap_fp32(float wx, float wy, float wz, float ax, float ay,
                                          float v1, float u2, float q, Sample& o) {
-    const CapCore k = cap_core<FLIP>(wx, wy, wz, ax, ay, v1, u2, q);
+    const CapCore k = cap_core<FRAME>(wx, wy, wz, ax, ay, v1, u2, q);
     // normalise and flip back
     const float t = k.s * k.invN;
     o.x = k.mx * t;
@@ -181,7 +188,7 @@ struct Reflected {
 template <bool FLIP = true>
 __device__ __forceinline__ bool cap_reflect_fp32(float wx, float wy, float wz, float ax, float ay,
                                                  float v1, float u2, float q, Reflected& o) {
-    const CapCore k = cap_core<FLIP>(wx, wy, wz, ax, ay, v1, u2, q);
+    const CapCore k = cap_core<FLIP ? kFrameFlip : kFrameUpper>(wx, wy, wz, ax, ay, v1, u2, q);
     const float inv_w = rsqrt_approx(fmaf(wx, wx, fmaf(wy, wy, wz * wz)));
     const float L = k.L2 * rsqrt_approx(k.L2) * inv_w;       // |M^-1 w| / |w|
     const float t = k.s * k.invN;
