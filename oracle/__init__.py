@@ -31,7 +31,7 @@ CFLAGS = ["-O2", "-std=c11", "-fPIC", "-shared", "-pthread", "-ffp-contract=off"
 def build(force: bool = False) -> str:
     """Compile oracle.c into liboracle.so (gcc).  Returns the library path."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        cmd = ["gcc", *CFLAGS, _SRC, "-o", _LIB, "-lm"]
+        cmd = ["gcc", *CFLAGS, _SRC, "-o", _LIB, "-lquadmath", "-lm"]
         subprocess.run(cmd, check=True)
     return _LIB
 

@@ -32,6 +32,7 @@
 #include <stdlib.h>
 #include <string.h>
 #include <pthread.h>
+#include <quadmath.h>
 
 #define ORC_PI 3.14159265358979323846
 
@@ -174,16 +175,41 @@ void orc_sample_vndf(int method, const double wi_in[3], double ax, double ay,
 /* NEXT-3: the paper's NATIVE handling of incidence below the horizon (Fig. 4,
  * theta_i = 130 deg): Listing 1 + Listing 3 (or 2) applied as
  * printed to any wi with wi_std.z > -1 -- no flip.  The cap is (-ws.z, 1],
- * which for ws.z < 0 lies above z = |ws.z|. */
-void orc_sample_vndf_native(int method, const double wi_in[3], double ax, double ay,
-                            double u1, double u2, double h_out[3])
+ * which for ws.z < 0 lies above z = |ws.z|.
+ * Evaluated in binary128 (__float128): with wi nearly straight below and small
+ * alpha, ws.z = -1 + 1e-8 and Listing 3's h.z = z + wi.z is a
+ * difference of two numbers within 1e-15 of 1 -- beyond binary64, not beyond
+ * binary128 (reading R17).  Same literal steps as above. */
+typedef __float128 q128;
+void orc_sample_vndf_native(int method, const double wi_in[3], double ax_d, double ay_d,
+                            double u1_d, double u2_d, double h_out[3])
 {
-    v3 wi = mk(wi_in[0], wi_in[1], wi_in[2]);
-    v3 wi_std = normalize(mk(wi.x * ax, wi.y * ay, wi.z));
-    v3 wm_std = method == 0 ? hemisphere_cap(u1, u2, wi_std)
-                            : hemisphere_heitz(u1, u2, wi_std, NULL);
-    v3 wm = normalize(mk(wm_std.x * ax, wm_std.y * ay, wm_std.z));
-    h_out[0] = wm.x; h_out[1] = wm.y; h_out[2] = wm.z;
+    if (method != 0) {  /* Listing 2 needs no extra precision here (tests compare distributions) */
+        v3 wi = mk(wi_in[0], wi_in[1], wi_in[2]);
+        v3 wi_std = normalize(mk(wi.x * ax_d, wi.y * ay_d, wi.z));
+        v3 wm_std = hemisphere_heitz(u1_d, u2_d, wi_std, NULL);
+        v3 wm = normalize(mk(wm_std.x * ax_d, wm_std.y * ay_d, wm_std.z));
+        h_out[0] = wm.x; h_out[1] = wm.y; h_out[2] = wm.z;
+        return;
+    }
+    const q128 PI = M_PIq;
+    q128 ax = ax_d, ay = ay_d, u1 = u1_d, u2 = u2_d;
+    /* warp to the hemisphere configuration */
+    q128 tx = wi_in[0] * ax, ty = wi_in[1] * ay, tz = wi_in[2];
+    q128 L = sqrtq(tx * tx + ty * ty + tz * tz);
+    q128 wx = tx / L, wy = ty / L, wz = tz / L;
+    /* Listing 3 */
+    q128 phi = 2 * PI * u1;
+    q128 z = fmaq(1 - u2, 1 + wz, -wz);
+    q128 st2 = 1 - z * z;
+    if (st2 < 0) st2 = 0;
+    if (st2 > 1) st2 = 1;
+    q128 st = sqrtq(st2);
+    q128 hx = st * cosq(phi) + wx, hy = st * sinq(phi) + wy, hz = z + wz;
+    /* warp back with M^-T */
+    q128 mx = hx * ax, my = hy * ay, mz = hz;
+    q128 N = sqrtq(mx * mx + my * my + mz * mz);
+    h_out[0] = (double)(mx / N); h_out[1] = (double)(my / N); h_out[2] = (double)(mz / N);
 }
 
 /* ------------------------------------------------------------------------ */

@@ -29,10 +29,30 @@ def test_native_equals_flip_above_horizon(orc):
         ax, ay = np.exp(rng.uniform(np.log(0.01), 0, 2))
         u1, u2 = rng.uniform(0, 1, 2)
         for m in (CAP, HEITZ):
-            np.testing.assert_array_equal(orc.sample_vndf_native(m, wi, ax, ay, u1, u2),
-                                          orc.sample_vndf(m, wi, ax, ay, u1, u2))
+            # the native cap is evaluated in binary128 (reading R17): equal to rounding
+            np.testing.assert_allclose(orc.sample_vndf_native(m, wi, ax, ay, u1, u2),
+                                       orc.sample_vndf(m, wi, ax, ay, u1, u2), atol=1e-10)
         h = orc.sample_vndf(CAP, wi, ax, ay, u1, u2)
         assert orc.pdf_vndf_native(h, wi, ax, ay) == orc.pdf_vndf(h, wi, ax, ay)
+
+
+def test_native_quad_cap_resolves_straight_below(orc):
+    """Reading R17: at ws.z = -1 + 1e-8 the binary128 evaluation keeps h.z =
+    (1 - u2)(1 + ws.z) (the exact algebraic value of z + ws.z, Listing 3)."""
+    ax = ay = 1e-3
+    wi = np.array([0.187, -0.0439, -0.9813727])
+    wi /= np.linalg.norm(wi)
+    u1, u2 = 0.46373, 1 - 2**-24
+    h = orc.sample_vndf_native(CAP, wi, ax, ay, u1, u2)
+    t = np.array([ax * wi[0], ay * wi[1], wi[2]])
+    L = np.linalg.norm(t)
+    ws = t / L
+    a = (ws[0] ** 2 + ws[1] ** 2) / (1 - ws[2])       # 1 + ws.z without cancellation
+    hz = (1 - u2) * a
+    st = np.sqrt(u2 * ((1 - u2) * a * a + ws[0] ** 2 + ws[1] ** 2))
+    hs = np.array([st * np.cos(2 * np.pi * u1) + ws[0], st * np.sin(2 * np.pi * u1) + ws[1], hz])
+    m = np.array([ax * hs[0], ay * hs[1], hs[2]])
+    np.testing.assert_allclose(h, m / np.linalg.norm(m), atol=1e-9)
 
 
 @pytest.mark.parametrize("case", CASES, ids=[str(c) for c in CASES])
