@@ -201,6 +201,18 @@ vndf_status vndf_furnace(int method, float wi_x, float wi_y, float wi_z, float a
                          uint64_t seed, uint64_t first_index, int64_t n, double *sums,
                          vndf_stream_t stream);
 
+/* Distribution audit (NEXT-3): n samples of a fixed (wi, alpha), u1 = u(W0),
+ * u2 = u(W1) of the Philox block (counter j, key seed), binned on the device.
+ * method: 0 = spherical cap (reading R4), 1 = Heitz 2018, 2 = cap, native
+ * below-horizon handling.  mode 0: h in nt x nphi bins of (theta in [0, pi/2),
+ * phi in [0, 2 pi)) (expected masses: Eq. 1); mode 1: the std-space reflected
+ * direction c = reflect(ws, normalize(M^T h)) in bins of ((c.z + ws.z)/(1 + ws.z),
+ * phi_c/(2 pi)) -- uniform by Eq. 10.  Counts are ADDED to
+ * counts[nt * nphi] (device uint64), row-major in theta / z.  nt * nphi <= 8192. */
+vndf_status vndf_histogram(int method, int mode, float wi_x, float wi_y, float wi_z,
+                           float alpha_x, float alpha_y, uint64_t seed, uint64_t first_index,
+                           int64_t n, int nt, int nphi, uint64_t *counts, vndf_stream_t stream);
+
 /* Sampler-only microbenchmark in the paper's GPU methodology (P:814-817:
  * "calls Listing 1 64 times per lane").  Lane t (0 <= t < lanes) draws wi and
  * (alpha_x, alpha_y) once from the config-4 recipe of index t (seed), then for

@@ -29,7 +29,7 @@ SYMBOLS = (
     "vndf_sample_cap_pdf_host", "vndf_release_host_staging", "vndf_count_fixups", "vndf_count_fixups_philox",
     "vndf_set_launch_config", "vndf_status_string", "vndf_last_cuda_error", "vndf_version",
     "vndf_microbench", "vndf_sample_cap_reflect", "vndf_furnace", "vndf_pdf",
-    "vndf_sample_cap_pdf_native",
+    "vndf_sample_cap_pdf_native", "vndf_histogram",
 )
 
 
@@ -69,6 +69,8 @@ def lib() -> ctypes.CDLL:
         L.vndf_microbench.argtypes = [i32, u64, i64, i32, P, P]
         L.vndf_sample_cap_reflect.argtypes = [P] * 12 + [i64, P]
         L.vndf_pdf.argtypes = [P] * 9 + [i64, P]
+        f32_ = ctypes.c_float
+        L.vndf_histogram.argtypes = [i32, i32, f32_, f32_, f32_, f32_, f32_, u64, u64, i64, i32, i32, P, P]
         f32 = ctypes.c_float
         L.vndf_furnace.argtypes = [i32, f32, f32, f32, f32, f32, u64, u64, i64, P, P]
         L.vndf_status_string.argtypes = [i32]
@@ -273,6 +275,16 @@ def vndf_pdf(h_x, h_y, h_z, wi_x, wi_y, wi_z, alpha_x, alpha_y, pdf, n=None, str
     n = _n(n, h_x)
     _stream_call("vndf_pdf", (h_x, h_y, h_z, wi_x, wi_y, wi_z, alpha_x, alpha_y, pdf),
                  ("h_x", "h_y", "h_z", "wi_x", "wi_y", "wi_z", "alpha_x", "alpha_y", "pdf"), n, stream)
+
+
+def vndf_histogram(method, mode, wi, alpha, seed, n, nt, nphi, counts, first_index=0, stream=None):
+    """NEXT-3 device histogram (counts: int64 CUDA tensor of nt * nphi, added to)."""
+    import torch
+    p, dev = _dev_ptr(counts, int(nt) * int(nphi), "counts", dtype=torch.int64)
+    _check("vndf_histogram", lib().vndf_histogram(int(method), int(mode), float(wi[0]), float(wi[1]),
+                                                  float(wi[2]), float(alpha[0]), float(alpha[1]), int(seed),
+                                                  int(first_index), int(n), int(nt), int(nphi), p,
+                                                  _stream(stream, dev)))
 
 
 def vndf_furnace(method, wi, alpha, seed, n, sums, first_index=0, stream=None):

@@ -511,6 +511,77 @@ __global__ void furnace_finish_kernel(const double* __restrict__ partials, int b
     }
 }
 
+// ------------------------------------ NEXT-3: GPU histograms for chi-square --
+// Samples a fixed (wi, alpha) n times (u1 = u(W0), u2 = u(W1) of Philox block
+// (counter j, key seed)) and bins, in shared memory, either
+//   mode 0: h in (theta in [0, pi/2), phi in [0, 2 pi))  (compare with Eq. 1 masses)
+//   mode 1: the std-space reflected direction c = reflect(ws, normalize(M^T h'))
+//           in (u_z = (c.z + ws.z)/(1 + ws.z), phi_c / 2 pi): uniform by Eq. 10.
+// METHOD: kCap / kHeitz (reading R4 frame) or kCapNative.  Cap samples flagged
+// by the conditioning test are recomputed in float64 first, as in the product
+// kernels.  Counts are ADDED to counts[nt * nphi] (uint64).
+template <int METHOD>
+__global__ void __launch_bounds__(256) histogram_kernel(int mode, float wx, float wy, float wz, float ax,
+                                                        float ay, uint64_t seed, uint64_t first, int64_t n,
+                                                        int nt, int nphi, unsigned long long* counts) {
+    extern __shared__ unsigned int bins[];
+    const int nb = nt * nphi;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) bins[b] = 0u;
+    __syncthreads();
+    const bool native = METHOD == kCapNative;
+    const float s = (!native && wz < 0.0f) ? -1.0f : 1.0f;
+    // std-space incidence (for mode 1)
+    const float tx = ax * wx, ty = ay * wy;
+    const float iL = s * rsqrtf(fmaf(tx, tx, fmaf(ty, ty, wz * wz)));
+    const float wsx = tx * iL, wsy = ty * iL, wsz = wz * iL;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
+        const uint4 W = philox_sample(seed, first + (uint64_t)j);
+        const float v1 = fmaf(fw(W.x), 0x1p-24f, -0.5f);
+        const float f2 = fw(W.y);
+        const float u2 = f2 * 0x1p-24f, q = fmaf(f2, -0x1p-24f, 1.0f);
+        Sample o;
+        if (METHOD == kHeitz) {
+            heitz_fp32<false>(wx, wy, wz, ax, ay, v1, u2, o);
+        } else {
+            const bool f = native ? cap_fp32<false, kFrameNative>(wx, wy, wz, ax, ay, v1, u2, q, o)
+                                  : cap_fp32<false>(wx, wy, wz, ax, ay, v1, u2, q, o);
+            if (f) {
+                const float4 d = cap_fp64(wx, wy, wz, ax, ay, fw(W.x) * 0x1p-24f, u2, !native);
+                o.x = d.x;
+                o.y = d.y;
+                o.z = d.z;
+            }
+        }
+        int ib;
+        if (mode == 0) {
+            const float th = acosf(fminf(fmaxf(o.z, -1.0f), 1.0f));
+            float ph = atan2f(o.y, o.x);
+            if (ph < 0.0f) ph += 6.28318530717958648f;
+            const int it = min(max((int)(th * (float)nt * 0.636619772367581343f), 0), nt - 1);
+            const int ip = min(max((int)(ph * (float)nphi * 0.159154943091895336f), 0), nphi - 1);
+            ib = it * nphi + ip;
+        } else {
+            // h' = s h (sampling frame), hs ~ M^T h'
+            float hx = s * o.x / ax, hy = s * o.y / ay, hz = s * o.z;
+            const float ih = rsqrtf(fmaf(hx, hx, fmaf(hy, hy, hz * hz)));
+            hx *= ih; hy *= ih; hz *= ih;
+            const float d = 2.0f * fmaf(hx, wsx, fmaf(hy, wsy, hz * wsz));
+            const float cx = fmaf(d, hx, -wsx), cy = fmaf(d, hy, -wsy), cz = fmaf(d, hz, -wsz);
+            const float uz = (cz + wsz) / (1.0f + wsz);
+            float ph = atan2f(cy, cx);
+            if (ph < 0.0f) ph += 6.28318530717958648f;
+            const int it = min(max((int)(uz * (float)nt), 0), nt - 1);
+            const int ip = min(max((int)(ph * (float)nphi * 0.159154943091895336f), 0), nphi - 1);
+            ib = it * nphi + ip;
+        }
+        atomicAdd(&bins[ib], 1u);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb; b += blockDim.x)
+        if (bins[b]) atomicAdd(&counts[b], (unsigned long long)bins[b]);
+}
+
 // ------------------------------------- NEXT-1: sampler-only microbenchmark --
 // The paper's GPU methodology: each lane calls Listing 1 `iters`
 // times.  Lane t draws its incidence and roughness once from the config-4
@@ -1166,6 +1237,35 @@ vndf_status vndf_furnace(int method, float wi_x, float wi_y, float wi_z, float a
     }
     const cudaError_t ef = cudaFreeAsync(part, s);
     if (e == cudaSuccess) e = ef;
+    return e == cudaSuccess ? VNDF_OK : cuda_fail(e);
+}
+
+vndf_status vndf_histogram(int method, int mode, float wi_x, float wi_y, float wi_z, float alpha_x,
+                           float alpha_y, uint64_t seed, uint64_t first_index, int64_t n, int nt, int nphi,
+                           uint64_t* counts, vndf_stream_t stream) {
+    if (n < 0 || !counts || !aligned(counts, 8) || method < 0 || method > 2 || (mode != 0 && mode != 1) ||
+        nt < 1 || nphi < 1 || (int64_t)nt * nphi > 8192)
+        return VNDF_ERR_INVALID_ARGUMENT;
+    if (n == 0) return VNDF_OK;
+    const size_t smem = (size_t)nt * nphi * sizeof(unsigned int);
+    const void* k = method == 0 ? (const void*)histogram_kernel<kCap>
+                  : method == 1 ? (const void*)histogram_kernel<kHeitz>
+                                : (const void*)histogram_kernel<kCapNative>;
+    int dev = 0, sms = 0, occ = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, smem);
+    if (e != cudaSuccess) return cuda_fail(e);
+    const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sms * std::max(occ, 1));
+    cudaStream_t s = (cudaStream_t)stream;
+    auto* c = (unsigned long long*)counts;
+    if (method == 0)
+        histogram_kernel<kCap><<<grid, 256, smem, s>>>(mode, wi_x, wi_y, wi_z, alpha_x, alpha_y, seed, first_index, n, nt, nphi, c);
+    else if (method == 1)
+        histogram_kernel<kHeitz><<<grid, 256, smem, s>>>(mode, wi_x, wi_y, wi_z, alpha_x, alpha_y, seed, first_index, n, nt, nphi, c);
+    else
+        histogram_kernel<kCapNative><<<grid, 256, smem, s>>>(mode, wi_x, wi_y, wi_z, alpha_x, alpha_y, seed, first_index, n, nt, nphi, c);
+    e = cudaGetLastError();
     return e == cudaSuccess ? VNDF_OK : cuda_fail(e);
 }
 

@@ -287,8 +287,8 @@ __device__ __noinline__ void cap_reflect_fix_stream(const float* __restrict__ wx
 // Out-of-line entry for the streamed kernels: widening happens in here, so the
 // fp32 hot path carries no conversions for it.
 __device__ __noinline__ float4 cap_fp64(float wx, float wy, float wz, float ax, float ay, float u1,
-                                        float u2) {
-    return cap_fp64_d(wx, wy, wz, ax, ay, u1, u2);
+                                        float u2, bool flip = true) {
+    return cap_fp64_d(wx, wy, wz, ax, ay, u1, u2, flip);
 }
 
 // Streamed fix-up of sample i: re-reads its inputs (L2-resident: the chunk was
