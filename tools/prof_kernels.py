@@ -39,3 +39,20 @@ if which in ("all", "c4"):
         vndf.vndf_sample_heitz2018_philox(3, 0, n, *o)
     torch.cuda.synchronize()
 print("ok")
+
+if which in ("all", "next"):
+    cfg = synth.CONFIGS[2]
+    x = synth.fill(cfg.recipe, cfg.seed, cfg.n, device=dev)
+    ins = [x[k] for k in synth.PLANES]
+    ro = [torch.empty(cfg.n, device=dev) for _ in range(5)]
+    for _ in range(2):
+        vndf.vndf_sample_cap_reflect(*ins, *ro)
+        vndf.vndf_pdf(*ro[:3], *ins[:5], ro[3])
+    ck = torch.empty(148 * 2048 * 16, device=dev)
+    for m in (0, 1, 2):
+        vndf.vndf_microbench(m, 5, ck.numel(), 64, ck)
+    s = torch.zeros(2, dtype=torch.float64, device=dev)
+    for m in (0, 1):
+        vndf.vndf_furnace(m, (0.5, 0.2, 0.8426149773176359), (0.3, 0.1), 17, 1 << 26, s)
+    torch.cuda.synchronize()
+    print("next ok")
