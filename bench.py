@@ -392,7 +392,9 @@ def variants(torch, vndf, synth, dev, stream, x2, out2):
         _, per = time_launches(torch, lambda: vndf.vndf_microbench(method, 5, lanes, iters, ck, stream=stream),
                                100, 5, stream)
         med = sorted(per)[len(per) // 2]
-        mb[name] = {"gsamples_s": lanes * iters / med / 1e6, "median_ms": med}
+        gs = lanes * iters / med / 1e6
+        mb[name] = {"gsamples_s": gs, "median_ms": med,
+                    "roofline": issue_roofline(gs, f"microbench_{name}_warp_inst_per_sample")}
     mb["t_heitz_over_t_cap"] = mb["heitz"]["median_ms"] / mb["cap"]["median_ms"]
     mb["t_heitz_over_t_cap_literal"] = mb["heitz"]["median_ms"] / mb["cap_literal"]["median_ms"]
     mb["paper"] = "t_Heitz/t_cap 1.3925 on RTX 2080, 1.5296 on Arc A770 (P:814-821)"

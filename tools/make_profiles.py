@@ -64,6 +64,9 @@ for rep in reps:
                 return float(x) * mult
             traffic["cap_pdf_c2"] = int(val(d["dram__bytes_read.sum"]) + val(d["dram__bytes_write.sum"]))
 if traffic:
-    json.dump(traffic, open(os.path.join(ROOT, "profiles", "traffic.json"), "w"), indent=1)
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    merged = json.load(open(path)) if os.path.exists(path) else {}
+    merged.update(traffic)
+    json.dump(merged, open(path, "w"), indent=1)
 print(open(os.path.join(out, "launches_summary.md")).read())
 print(traffic)
