@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -112,6 +113,12 @@ __device__ __forceinline__ void st_stream<8>(float* p, const Vec<8>& r) {
                  : "memory");
 }
 
+// ------------------------------------------- programmatic dependent launch --
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ------------------------------------------------------------ one sample --
 // fp32 sample; returns the conditioning flag (always false for Heitz).
 template <int METHOD, bool PDF>
@@ -136,6 +143,11 @@ __device__ __forceinline__ void fix_one(const StreamArgs& a, bool pdf, int64_t i
 // deferral: the vector loop itself stays call-free).
 template <int METHOD, bool PDF, int V>
 __global__ void __launch_bounds__(256) stream_kernel(StreamArgs a, int64_t n) {
+    // Programmatic dependent launch: let the next kernel on the stream be
+    // scheduled once every block of this grid is running, and wait for the
+    // previous grid (its completion and memory flush) before touching memory.
+    pdl_launch_dependents();
+    pdl_wait();
     const int64_t nchunks = n / V;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -653,6 +665,29 @@ LaunchPrefs prefs() {
     return g_prefs;
 }
 
+// Launch with the programmatic-stream-serialization attribute (PDL): the
+// kernel may start while the previous kernel on the stream drains; it calls
+// griddepcontrol.wait before its first memory access, so stream order holds.
+// Disabled with vector_width/block_size knobs untouched via VNDF_NO_PDL=1.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, cudaStream_t s, Args... args) {
+    static const bool off = [] {
+        const char* v = getenv("VNDF_NO_PDL");
+        return v && v[0] == '1';
+    }();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = off ? 0 : 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 // Persistent grid: min(work, SMs x resident blocks per SM).
 // persistent: default grid policy of the kernel family when no preference is
 // set (streamed kernels: one chunk per thread, measured faster on B200 for
@@ -788,7 +823,8 @@ vndf_status launch_stream_v(const StreamArgs& a, int64_t n, cudaStream_t s) {
     int grid = 0;
     cudaError_t e = grid_for(k, block, std::max<int64_t>(n / V, 1), &grid, /*persistent=*/false);
     if (e != cudaSuccess) return cuda_fail(e);
-    stream_kernel<METHOD, PDF, V><<<grid, block, 0, s>>>(a, n);
+    e = launch_pdl(stream_kernel<METHOD, PDF, V>, grid, block, s, a, n);
+    if (e != cudaSuccess) return cuda_fail(e);
     e = cudaGetLastError();
     return e == cudaSuccess ? VNDF_OK : cuda_fail(e);
 }
