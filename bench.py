@@ -159,22 +159,31 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ timed loops ---
-def time_launches(torch, fn, steps: int, warmup: int, stream, barrier=None):
+def time_launches(torch, fn, steps: int, warmup: int, stream, barrier=None, per_step: bool = True):
     """W untimed warm-up launches, then `steps` launches bracketed by events on
-    `stream`.  Returns (total_ms, per_launch_ms list)."""
+    `stream`.  Returns (total_ms, per_launch_ms list).  per_step=False records
+    only the two bracketing events: an event recorded between two launches
+    stops the next launch from overlapping the previous one's tail
+    (programmatic dependent launch), which a back-to-back workload does not pay."""
     for _ in range(warmup):
         fn()
     if barrier:
         barrier()
     torch.cuda.synchronize()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range((steps if per_step else 1) + 1)]
     ev[0].record(stream)
     for k in range(steps):
         fn()
-        ev[k + 1].record(stream)
+        if per_step:
+            ev[k + 1].record(stream)
+    if not per_step:
+        ev[1].record(stream)
     torch.cuda.synchronize()
-    per = [ev[k].elapsed_time(ev[k + 1]) for k in range(steps)]
-    return ev[0].elapsed_time(ev[steps]), per
+    if per_step:
+        per = [ev[k].elapsed_time(ev[k + 1]) for k in range(steps)]
+        return ev[0].elapsed_time(ev[steps]), per
+    total = ev[0].elapsed_time(ev[1])
+    return total, [total / steps] * steps
 
 
 def cpu_baseline(host_planes, n_sample: int, budget_s: float = 12.0):
@@ -257,7 +266,7 @@ def run_ours(args):
         barrier()
     torch.cuda.synchronize()
     clocks.start()
-    total_ms, per = time_launches(torch, step, args.steps, 0, stream)
+    total_ms, per = time_launches(torch, step, args.steps, 0, stream, per_step=False)
     clocks.stop()
     if barrier:
         barrier()
@@ -316,7 +325,7 @@ def variants(torch, vndf, synth, dev, stream, x2, out2):
     reps, warm = 10, 3
 
     def timed(fn):
-        total, per = time_launches(torch, fn, reps, warm, stream)
+        total, per = time_launches(torch, fn, reps, warm, stream, per_step=False)
         return total / reps
 
     n2 = x2["wi_x"].numel()
