@@ -369,6 +369,8 @@ struct PdfArgs {
 // 32 B in (h, wi, alpha), 4 B out per sample; HBM-bound.
 template <int V>
 __global__ void __launch_bounds__(256) pdf_kernel(PdfArgs a, int64_t n) {
+    pdl_launch_dependents();
+    pdl_wait();
     const int64_t nchunks = n / V;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -408,6 +410,8 @@ struct ReflectArgs {
 // Streamed: 28 B in, 20 B out per sample (wo.xyz, pdf Eq. 20, weight G2/G1).
 template <int V>
 __global__ void __launch_bounds__(256) reflect_kernel(ReflectArgs a, int64_t n) {
+    pdl_launch_dependents();
+    pdl_wait();
     const int64_t nchunks = n / V;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1194,15 +1198,15 @@ vndf_status vndf_sample_cap_reflect(const float* wi_x, const float* wi_y, const 
     switch (v) {
         case 8:
             e = grid_for((const void*)reflect_kernel<8>, block, std::max<int64_t>(n / 8, 1), &grid, false);
-            if (e == cudaSuccess) reflect_kernel<8><<<grid, block, 0, s>>>(a, n);
+            if (e == cudaSuccess) e = launch_pdl(reflect_kernel<8>, grid, block, s, a, n);
             break;
         case 4:
             e = grid_for((const void*)reflect_kernel<4>, block, std::max<int64_t>(n / 4, 1), &grid, false);
-            if (e == cudaSuccess) reflect_kernel<4><<<grid, block, 0, s>>>(a, n);
+            if (e == cudaSuccess) e = launch_pdl(reflect_kernel<4>, grid, block, s, a, n);
             break;
         default:
             e = grid_for((const void*)reflect_kernel<1>, block, n, &grid, false);
-            if (e == cudaSuccess) reflect_kernel<1><<<grid, block, 0, s>>>(a, n);
+            if (e == cudaSuccess) e = launch_pdl(reflect_kernel<1>, grid, block, s, a, n);
     }
     if (e == cudaSuccess) e = cudaGetLastError();
     return e == cudaSuccess ? VNDF_OK : cuda_fail(e);
@@ -1230,15 +1234,15 @@ vndf_status vndf_pdf(const float* h_x, const float* h_y, const float* h_z, const
     switch (v) {
         case 8:
             e = grid_for((const void*)pdf_kernel<8>, block, std::max<int64_t>(n / 8, 1), &grid, false);
-            if (e == cudaSuccess) pdf_kernel<8><<<grid, block, 0, s>>>(a, n);
+            if (e == cudaSuccess) e = launch_pdl(pdf_kernel<8>, grid, block, s, a, n);
             break;
         case 4:
             e = grid_for((const void*)pdf_kernel<4>, block, std::max<int64_t>(n / 4, 1), &grid, false);
-            if (e == cudaSuccess) pdf_kernel<4><<<grid, block, 0, s>>>(a, n);
+            if (e == cudaSuccess) e = launch_pdl(pdf_kernel<4>, grid, block, s, a, n);
             break;
         default:
             e = grid_for((const void*)pdf_kernel<1>, block, n, &grid, false);
-            if (e == cudaSuccess) pdf_kernel<1><<<grid, block, 0, s>>>(a, n);
+            if (e == cudaSuccess) e = launch_pdl(pdf_kernel<1>, grid, block, s, a, n);
     }
     if (e == cudaSuccess) e = cudaGetLastError();
     return e == cudaSuccess ? VNDF_OK : cuda_fail(e);
