@@ -137,17 +137,32 @@ __device__ __forceinline__ void fix_one(const StreamArgs& a, bool pdf, int64_t i
 
 // ------------------------------------------------------- streamed kernel --
 // Chunk c covers samples [c V, c V + V).  Full chunks go through the vector
-// path on a persistent grid-stride loop; the n mod V tail is done by the
-// first threads of the grid with scalar accesses.  Flagged samples of a
-// chunk are recomputed in float64 after the chunk's stores (in-thread
-// deferral: the vector loop itself stays call-free).
+// path (one chunk per thread by default, grid-stride if the grid is capped);
+// the n mod V tail is done by the first threads of the grid with scalar
+// accesses.  Flagged samples are pushed to a block-level shared-memory queue
+// and recomputed in float64 after a block barrier, one per thread, so a
+// block's few fix-ups (~3.5 per 1024 samples in config 5) run side by side
+// instead of serialising their warps; the vector loop itself stays call-free.
+// A queue overflow (only possible with a capped, grid-stride grid) falls back
+// to fixing in the thread that found it.
+constexpr int kBlockFixCap = 512;
+
 template <int METHOD, bool PDF, int V>
 __global__ void __launch_bounds__(256) stream_kernel(StreamArgs a, int64_t n) {
+    __shared__ int64_t fix_idx[METHOD != kHeitz ? kBlockFixCap : 1];
+    __shared__ int fix_count;
+    if (METHOD != kHeitz && threadIdx.x == 0) fix_count = 0;
     // Programmatic dependent launch: let the next kernel on the stream be
     // scheduled once every block of this grid is running, and wait for the
     // previous grid (its completion and memory flush) before touching memory.
     pdl_launch_dependents();
     pdl_wait();
+    if (METHOD != kHeitz) __syncthreads();
+    auto defer = [&](int64_t i) {
+        const int slot = atomicAdd(&fix_count, 1);
+        if (slot < kBlockFixCap) fix_idx[slot] = i;
+        else fix_one(a, PDF, i, METHOD == kCap);
+    };
     const int64_t nchunks = n / V;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -178,7 +193,7 @@ __global__ void __launch_bounds__(256) stream_kernel(StreamArgs a, int64_t n) {
             do {
                 const int j = __ffs(flags) - 1;
                 flags &= flags - 1;
-                fix_one(a, PDF, i + j, METHOD == kCap);
+                defer(i + j);
             } while (flags);
         }
     }
@@ -192,8 +207,13 @@ __global__ void __launch_bounds__(256) stream_kernel(StreamArgs a, int64_t n) {
             a.hy[i] = o.y;
             a.hz[i] = o.z;
             if (PDF) a.pdf[i] = o.pdf;
-            if (METHOD != kHeitz && f) fix_one(a, PDF, i, METHOD == kCap);
+            if (METHOD != kHeitz && f) defer(i);
         }
+    }
+    if (METHOD != kHeitz) {
+        __syncthreads();
+        const int m = min(fix_count, kBlockFixCap);
+        for (int t = threadIdx.x; t < m; t += blockDim.x) fix_one(a, PDF, fix_idx[t], METHOD == kCap);
     }
 }
 
