@@ -23,6 +23,8 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <vector>
+#include <cmath>
 
 #include "vndf_device.cuh"
 #include "../../include/vndf.h"
@@ -119,6 +121,36 @@ __device__ __forceinline__ void pdl_launch_dependents() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// ------------------------------------------ TMA bulk copy into shared memory --
+// One elected thread arms an mbarrier with the expected byte count and issues
+// cp.async.bulk (global -> shared, SASS UBLKCP); every thread waits on the
+// barrier's phase 0.  `bytes` must be a multiple of 16, both addresses 16-byte
+// aligned.
+__device__ __forceinline__ void bulk_load_shared(void* smem_dst, const void* gmem_src, uint32_t bytes,
+                                                 uint64_t* bar) {
+    const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(d), "l"(gmem_src), "r"(bytes), "r"(b)
+                     : "memory");
+    }
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(b)
+            : "memory");
+    }
+}
+
 // ------------------------------------------------------------ one sample --
 // fp32 sample; returns the conditioning flag (always false for Heitz).
 template <int METHOD, bool PDF>
@@ -147,8 +179,12 @@ __device__ __forceinline__ void fix_one(const StreamArgs& a, bool pdf, int64_t i
 // to fixing in the thread that found it.
 constexpr int kBlockFixCap = 512;
 
+#ifndef VNDF_STREAM_MINB
+#define VNDF_STREAM_MINB 1
+#endif
+
 template <int METHOD, bool PDF, int V>
-__global__ void __launch_bounds__(256) stream_kernel(StreamArgs a, int64_t n) {
+__global__ void __launch_bounds__(256, VNDF_STREAM_MINB) stream_kernel(StreamArgs a, int64_t n) {
     __shared__ int64_t fix_idx[METHOD != kHeitz ? kBlockFixCap : 1];
     __shared__ int fix_count;
     if (METHOD != kHeitz && threadIdx.x == 0) fix_count = 0;
@@ -232,8 +268,8 @@ struct FixQueue {
 
 template <int METHOD, bool PDF>
 __device__ __forceinline__ Sample philox_one(uint64_t seed, uint64_t first, uint64_t k,
-                                             const FixQueue& fq) {
-    const Inputs in = c4_inputs_fp32(philox_sample(seed, first + k));
+                                             const FixQueue& fq, const float2* __restrict__ tab) {
+    const Inputs in = c4_inputs_fp32(philox_sample(seed, first + k), tab);
     Sample o;
     if (METHOD == kCap) {
         // config-4 inputs are on the upper hemisphere (wi.z = 1 - u > 0): no flip
@@ -249,7 +285,8 @@ __device__ __forceinline__ Sample philox_one(uint64_t seed, uint64_t first, uint
 }
 
 __global__ void __launch_bounds__(128) philox_fixup_kernel(uint64_t seed, uint64_t first, int64_t n,
-                                                            FixQueue fq, float* __restrict__ hx,
+                                                            FixQueue fq, const float2* __restrict__ gtab,
+                                                            float* __restrict__ hx,
                                                             float* __restrict__ hy, float* __restrict__ hz,
                                                             float* __restrict__ pdf) {
     const uint64_t count = *fq.count;
@@ -267,7 +304,7 @@ __global__ void __launch_bounds__(128) philox_fixup_kernel(uint64_t seed, uint64
         return;
     }
     for (uint64_t k = t0; k < (uint64_t)n; k += stride) {  // overflow: rescan
-        const Inputs in = c4_inputs_fp32(philox_sample(seed, first + k));
+        const Inputs in = c4_inputs_fp32(philox_sample(seed, first + k), gtab);
         Sample o;
         if (cap_fp32<true, kFrameUpper>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o)) {
             const float4 f = cap_philox_fp64(seed, first + k);
@@ -290,7 +327,12 @@ template <int METHOD, bool PDF, int V>
 __global__ void __launch_bounds__(256, VNDF_PHILOX_MINB) philox_kernel(uint64_t seed, uint64_t first, int64_t n,
                                                      float* __restrict__ hxp, float* __restrict__ hyp,
                                                      float* __restrict__ hzp, float* __restrict__ pdfp,
-                                                     FixQueue fq) {
+                                                     FixQueue fq, const float2* __restrict__ gtab) {
+    // Stage the 64 KB sin/cos table of the incidence azimuth in shared memory
+    // with one TMA bulk copy (cp.async.bulk, completion on an mbarrier).
+    extern __shared__ __align__(16) float2 tab[];
+    __shared__ __align__(8) uint64_t tab_bar;
+    bulk_load_shared(tab, gtab, kSinCosTableEntries * sizeof(float2), &tab_bar);
     const int64_t nchunks = n / V;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -299,7 +341,7 @@ __global__ void __launch_bounds__(256, VNDF_PHILOX_MINB) philox_kernel(uint64_t 
         Vec<V> hx, hy, hz, pd;
 #pragma unroll
         for (int j = 0; j < V; ++j) {
-            const Sample o = philox_one<METHOD, PDF>(seed, first, (uint64_t)(i + j), fq);
+            const Sample o = philox_one<METHOD, PDF>(seed, first, (uint64_t)(i + j), fq, tab);
             hx.v[j] = o.x;
             hy.v[j] = o.y;
             hz.v[j] = o.z;
@@ -313,7 +355,7 @@ __global__ void __launch_bounds__(256, VNDF_PHILOX_MINB) philox_kernel(uint64_t 
     if (V > 1) {
         const int64_t i = nchunks * V + tid;
         if (i < n) {
-            const Sample o = philox_one<METHOD, PDF>(seed, first, (uint64_t)i, fq);
+            const Sample o = philox_one<METHOD, PDF>(seed, first, (uint64_t)i, fq, tab);
             hxp[i] = o.x;
             hyp[i] = o.y;
             hzp[i] = o.z;
@@ -357,6 +399,7 @@ __global__ void __launch_bounds__(256) count_stream_kernel(StreamArgs a, int64_t
 }
 
 __global__ void __launch_bounds__(256) count_philox_kernel(uint64_t seed, uint64_t first, int64_t n,
+                                                           const float2* __restrict__ gtab,
                                                            unsigned long long* count) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t start = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -365,9 +408,9 @@ __global__ void __launch_bounds__(256) count_philox_kernel(uint64_t seed, uint64
         const int64_t i = start + r * stride;
         bool flag = false;
         if (i < n) {
-            const Inputs in = c4_inputs_fp32(philox_sample(seed, first + (uint64_t)i));
+            const Inputs in = c4_inputs_fp32(philox_sample(seed, first + (uint64_t)i), gtab);
             Sample o;
-            flag = cap_fp32<true>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o);
+            flag = cap_fp32<true, kFrameUpper>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o);
         }
         warp_count(flag, count);
     }
@@ -634,11 +677,12 @@ constexpr float kRotC = 0.764842187f, kRotS = 0.644217687f;  // cos, sin of 0.7 
 
 template <int VARIANT>
 __global__ void __launch_bounds__(256) microbench_kernel(uint64_t seed, int64_t lanes, int iters,
+                                                         const float2* __restrict__ gtab,
                                                          float* __restrict__ checksum) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= lanes) return;
     const uint4 W = philox_sample(seed, (uint64_t)t);
-    const Inputs in = c4_inputs_fp32(W);
+    const Inputs in = c4_inputs_fp32(W, gtab);
     uint32_t x1 = W.x, x2 = W.y;
     float wx = in.wx, wy = in.wy;
     float acc = 0.0f;
@@ -789,6 +833,39 @@ cudaError_t queue_alloc(void** p, size_t bytes, cudaStream_t s) {
     return cudaMallocFromPoolAsync(p, bytes, pool, s);
 }
 
+// Octant table of (sin, cos)(2 pi j / 2^16), j = 0 .. 8192, for the config-4
+// incidence azimuth: built on the host in float64 (correctly rounded to fp32),
+// uploaded once per device, kept for the life of the process (64 KB).
+std::map<int, float2*> g_sincos_tab;
+
+cudaError_t sincos_table(float2** out) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_sincos_tab.find(dev);
+    if (it != g_sincos_tab.end()) {
+        *out = it->second;
+        return cudaSuccess;
+    }
+    std::vector<float2> h(kSinCosTableEntries);
+    for (int j = 0; j < kSinCosTableEntries; ++j) {
+        const int jj = j < 8193 ? j : 8192;  // padding entry repeats the last one
+        const double a = 2.0 * 3.14159265358979323846 * (double)jj / 65536.0;
+        h[j] = make_float2((float)sin(a), (float)cos(a));
+    }
+    float2* d = nullptr;
+    e = cudaMalloc((void**)&d, h.size() * sizeof(float2));
+    if (e == cudaSuccess) e = cudaMemcpy(d, h.data(), h.size() * sizeof(float2), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        if (d) cudaFree(d);
+        return e;
+    }
+    g_sincos_tab[dev] = d;
+    *out = d;
+    return cudaSuccess;
+}
+
 int block_size(int dflt = 256) {
     const int b = prefs().block_size;
     return b > 0 ? b : dflt;
@@ -908,7 +985,18 @@ vndf_status launch_philox_v(uint64_t seed, uint64_t first, int64_t n, float* hx,
             return cuda_fail(e);
         }
     }
-    philox_kernel<METHOD, PDF, V><<<grid, block, 0, s>>>(seed, first, n, hx, hy, hz, pdf, fq);
+    float2* gtab = nullptr;
+    e = sincos_table(&gtab);
+    if (e != cudaSuccess) {
+        if (qbuf) cudaFreeAsync(qbuf, s);
+        return cuda_fail(e);
+    }
+    const size_t smem = kSinCosTableEntries * sizeof(float2);
+    static std::once_flag attr_once;
+    std::call_once(attr_once, [&] {
+        cudaFuncSetAttribute(philox_kernel<METHOD, PDF, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    });
+    philox_kernel<METHOD, PDF, V><<<grid, block, smem, s>>>(seed, first, n, hx, hy, hz, pdf, fq, gtab);
     e = cudaGetLastError();
     if (e == cudaSuccess && METHOD == kCap) {
         // one thread per queue slot up to SMs x 32 blocks; blocks past the
@@ -917,7 +1005,7 @@ vndf_status launch_philox_v(uint64_t seed, uint64_t first, int64_t n, float* hx,
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const int64_t fix_blocks = std::min<int64_t>(((int64_t)fq.cap + 127) / 128, (int64_t)std::max(sms, 1) * 32);
-        philox_fixup_kernel<<<(int)fix_blocks, 128, 0, s>>>(seed, first, n, fq, hx, hy, hz, pdf);
+        philox_fixup_kernel<<<(int)fix_blocks, 128, 0, s>>>(seed, first, n, fq, gtab, hx, hy, hz, pdf);
         e = cudaGetLastError();
     }
     if (qbuf) {
@@ -1118,7 +1206,10 @@ vndf_status vndf_count_fixups_philox(uint64_t seed, uint64_t first_index, int64_
     int grid = 0;
     cudaError_t e = grid_for((const void*)count_philox_kernel, 256, n, &grid);
     if (e != cudaSuccess) return cuda_fail(e);
-    count_philox_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(seed, first_index, n,
+    float2* gtab = nullptr;
+    e = sincos_table(&gtab);
+    if (e != cudaSuccess) return cuda_fail(e);
+    count_philox_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(seed, first_index, n, gtab,
                                                                  (unsigned long long*)count);
     e = cudaGetLastError();
     return e == cudaSuccess ? VNDF_OK : cuda_fail(e);
@@ -1338,12 +1429,15 @@ vndf_status vndf_microbench(int method, uint64_t seed, int64_t lanes, int iters,
     const int64_t grid = (lanes + block - 1) / block;
     if (grid > INT32_MAX) return VNDF_ERR_INVALID_ARGUMENT;
     cudaStream_t s = (cudaStream_t)stream;
+    float2* gtab = nullptr;
+    cudaError_t e = sincos_table(&gtab);
+    if (e != cudaSuccess) return cuda_fail(e);
     switch (method) {
-        case 0: microbench_kernel<0><<<(int)grid, block, 0, s>>>(seed, lanes, iters, checksum); break;
-        case 1: microbench_kernel<1><<<(int)grid, block, 0, s>>>(seed, lanes, iters, checksum); break;
-        default: microbench_kernel<2><<<(int)grid, block, 0, s>>>(seed, lanes, iters, checksum); break;
+        case 0: microbench_kernel<0><<<(int)grid, block, 0, s>>>(seed, lanes, iters, gtab, checksum); break;
+        case 1: microbench_kernel<1><<<(int)grid, block, 0, s>>>(seed, lanes, iters, gtab, checksum); break;
+        default: microbench_kernel<2><<<(int)grid, block, 0, s>>>(seed, lanes, iters, gtab, checksum); break;
     }
-    const cudaError_t e = cudaGetLastError();
+    e = cudaGetLastError();
     return e == cudaSuccess ? VNDF_OK : cuda_fail(e);
 }
 

@@ -484,7 +484,27 @@ __device__ __forceinline__ uint4 philox_sample(uint64_t seed, uint64_t i) {
                          make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
 }
 
-__device__ __forceinline__ Inputs c4_inputs_fp32(uint4 W) {
+// sin and cos of 2 pi K / 2^16 for a 16-bit K from the octant table
+// T[j] = (sin, cos)(2 pi j / 2^16), j = 0 .. 8192 (correctly rounded fp32,
+// built on the host in float64): quadrant q = K >> 14, rq = K mod 2^14,
+// j = min(rq, 2^14 - rq); swap sin/cos when rq > 2^13 XOR q odd; signs by
+// quadrant.  Exact reduction, ~0.5 ulp: relative accuracy in each component.
+constexpr int kSinCosTableEntries = 8194;  // 8193 used, padded to a 16-byte multiple
+__device__ __forceinline__ void sincos_2pi_u16(uint32_t K, const float2* __restrict__ tab, float* s,
+                                               float* c) {
+    const uint32_t q = K >> 14, rq = K & 0x3FFFu;
+    const uint32_t j = min(rq, 16384u - rq);
+    const float2 t = tab[j];
+    const bool swap = (rq > 8192u) != ((q & 1u) != 0u);
+    const float a = swap ? t.y : t.x, b = swap ? t.x : t.y;
+    *s = (q & 2u) ? -a : a;
+    *c = ((q + 1u) & 2u) ? -b : b;
+}
+
+// tab = nullptr: sincospif; else the 16-bit table (shared or global memory).
+// (A compile-time switch: the product kernels always pass the table.)
+template <bool TABLE = true>
+__device__ __forceinline__ Inputs c4_inputs_fp32(uint4 W, const float2* __restrict__ tab) {
     Inputs in;
     const float fa = fw16(W.x, W.y);
     const float ua = fa * 0x1p-16f;
@@ -493,9 +513,14 @@ __device__ __forceinline__ Inputs c4_inputs_fp32(uint4 W) {
     // wi needs RELATIVE accuracy in each component: the stretch multiplies an
     // absolute error of wi.x, wi.y by up to max(a)/|M^-1 wi|, which is large at
     // grazing incidence.  sincospif (exact reduction in units of pi, ~1 ulp)
-    // gives that; MUFU.SIN/COS (absolute error 2^-21.4) would not.
+    // or the correctly rounded 16-bit table give that; MUFU.SIN/COS (absolute
+    // error 2^-21.4) would not.
     float sp, cp;
-    sincospif(fw16(W.z, W.w) * 0x1p-15f, &sp, &cp);     // 2 pi ub, ub = fw16 2^-16
+    if (TABLE) {
+        sincos_2pi_u16(__byte_perm(W.z, W.w, 0x7740) & 0xFFFFu, tab, &sp, &cp);
+    } else {
+        sincospif(fw16(W.z, W.w) * 0x1p-15f, &sp, &cp);  // 2 pi ub, ub = fw16 2^-16
+    }
     in.wx = r * cp;
     in.wy = r * sp;
     in.wz = z;
