@@ -578,15 +578,29 @@ __global__ void __launch_bounds__(256) furnace_kernel(float wx, float wy, float 
     }
 }
 
-__global__ void furnace_finish_kernel(const double* __restrict__ partials, int blocks, double* out) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        double a1 = 0.0, a2 = 0.0;
-        for (int b = 0; b < blocks; ++b) {
-            a1 += partials[2 * b];
-            a2 += partials[2 * b + 1];
+__global__ void __launch_bounds__(256) furnace_finish_kernel(const double* __restrict__ partials, int blocks,
+                                                            double* out) {
+    // fixed-order reduction (deterministic for a given grid): strided partial
+    // sums per thread, then a shared-memory tree
+    __shared__ double r1[256], r2[256];
+    double a1 = 0.0, a2 = 0.0;
+    for (int b = threadIdx.x; b < blocks; b += blockDim.x) {
+        a1 += partials[2 * b];
+        a2 += partials[2 * b + 1];
+    }
+    r1[threadIdx.x] = a1;
+    r2[threadIdx.x] = a2;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) {
+            r1[threadIdx.x] += r1[threadIdx.x + w];
+            r2[threadIdx.x] += r2[threadIdx.x + w];
         }
-        out[0] = a1;
-        out[1] = a2;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        out[0] = r1[0];
+        out[1] = r2[0];
     }
 }
 
@@ -1383,7 +1397,7 @@ vndf_status vndf_furnace(int method, float wi_x, float wi_y, float wi_z, float a
                                                     n, (double*)part);
     e = cudaGetLastError();
     if (e == cudaSuccess) {
-        furnace_finish_kernel<<<1, 32, 0, s>>>((const double*)part, grid, sums);
+        furnace_finish_kernel<<<1, 256, 0, s>>>((const double*)part, grid, sums);
         e = cudaGetLastError();
     }
     const cudaError_t ef = cudaFreeAsync(part, s);

@@ -57,7 +57,8 @@ for rep in reps:
                 if k != "kernel":
                     f.write(f"    {k:85s} {v}\n")
     for d in res:
-        if "stream_kernel<0, 1, 8>" in d["kernel"] and "dram__bytes_read.sum" in d:
+        if ("stream_kernel<0, 1, 8>" in d["kernel"] and "dram__bytes_read.sum" in d
+                and d.get("launch__grid_size", "").strip() == "16384"):  # config 2: 2^24 / 8 / 128
             def val(s):
                 x, u = s.split()[0], s.split()[1] if len(s.split()) > 1 else "byte"
                 mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u]
