@@ -23,6 +23,7 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <utility>
 #include <vector>
 #include <cmath>
 
@@ -774,7 +775,8 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, cudaStream
 // persistent: default grid policy of the kernel family when no preference is
 // set (streamed kernels: one chunk per thread, measured faster on B200 for
 // HBM-bound work; fused Philox: persistent, occupancy-limited).
-cudaError_t grid_for(const void* kernel, int block, int64_t work_items, int* grid, bool persistent = true) {
+cudaError_t grid_for(const void* kernel, int block, int64_t work_items, int* grid, bool persistent = true,
+                     size_t smem = 0) {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
@@ -793,7 +795,7 @@ cudaError_t grid_for(const void* kernel, int block, int64_t work_items, int* gri
         g_sms[dev] = sms;
     }
     if (occ == 0) {
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, block, 0);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, block, smem);
         if (e != cudaSuccess) return e;
         if (occ < 1) occ = 1;
         std::lock_guard<std::mutex> lk(g_mu);
@@ -845,6 +847,22 @@ cudaError_t queue_alloc(void** p, size_t bytes, cudaStream_t s) {
         }
     }
     return cudaMallocFromPoolAsync(p, bytes, pool, s);
+}
+
+// Opt a kernel into > 48 KB of dynamic shared memory, once per (device, kernel):
+// function attributes are per device, a process may drive several.
+std::map<std::pair<int, const void*>, bool> g_smem_attr;
+
+cudaError_t allow_dynamic_smem(const void* kernel, size_t bytes) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(g_mu);
+    const auto key = std::make_pair(dev, kernel);
+    if (g_smem_attr.count(key)) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) g_smem_attr[key] = true;
+    return e;
 }
 
 // Octant table of (sin, cos)(2 pi j / 2^16), j = 0 .. 8192, for the config-4
@@ -981,8 +999,11 @@ vndf_status launch_philox_v(uint64_t seed, uint64_t first, int64_t n, float* hx,
                             float* pdf, cudaStream_t s) {
     const void* k = (const void*)philox_kernel<METHOD, PDF, V>;
     const int block = block_size();
+    const size_t smem = kSinCosTableEntries * sizeof(float2);
+    cudaError_t e = allow_dynamic_smem(k, smem);
+    if (e != cudaSuccess) return cuda_fail(e);
     int grid = 0;
-    cudaError_t e = grid_for(k, block, std::max<int64_t>(n / V, 1), &grid);
+    e = grid_for(k, block, std::max<int64_t>(n / V, 1), &grid, true, smem);
     if (e != cudaSuccess) return cuda_fail(e);
     FixQueue fq{nullptr, nullptr, 0};
     void* qbuf = nullptr;
@@ -1005,11 +1026,6 @@ vndf_status launch_philox_v(uint64_t seed, uint64_t first, int64_t n, float* hx,
         if (qbuf) cudaFreeAsync(qbuf, s);
         return cuda_fail(e);
     }
-    const size_t smem = kSinCosTableEntries * sizeof(float2);
-    static std::once_flag attr_once;
-    std::call_once(attr_once, [&] {
-        cudaFuncSetAttribute(philox_kernel<METHOD, PDF, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    });
     philox_kernel<METHOD, PDF, V><<<grid, block, smem, s>>>(seed, first, n, hx, hy, hz, pdf, fq, gtab);
     e = cudaGetLastError();
     if (e == cudaSuccess && METHOD == kCap) {
