@@ -14,7 +14,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libvndf.so")
 SOURCES = [os.path.join(CSRC, "vndf.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "vndf_device.cuh"), os.path.join(ROOT, "include", "vndf.h")]
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")] + [
+    os.path.join(ROOT, "include", "vndf.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 NVCC_FLAGS = [

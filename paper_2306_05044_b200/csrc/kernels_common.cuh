@@ -1,0 +1,140 @@
+// kernels_common.cuh -- device helpers shared by the kernels: argument structs, streaming
+// vector loads/stores, programmatic dependent launch, TMA bulk copy, the
+// per-sample dispatch.
+// Part of libvndf's single translation unit (included by vndf.cu inside its
+// anonymous namespace); see vndf.cu for the kernel list and DESIGN.md s.6.
+#pragma once
+
+// kCapNative: the paper's native below-horizon handling (NEXT-3, no flip)
+enum Method { kCap = 0, kHeitz = 1, kCapNative = 2 };
+
+struct StreamArgs {
+    const float* wx;
+    const float* wy;
+    const float* wz;
+    const float* ax;
+    const float* ay;
+    const float* u1;
+    const float* u2;
+    float* hx;
+    float* hy;
+    float* hz;
+    float* pdf;
+};
+
+// ---------------------------------------------------------------- memory ops
+// Streaming loads: read-only path, no L1 allocation (each byte is read once).
+template <int V>
+struct Vec {
+    float v[V];
+};
+
+template <int V>
+__device__ __forceinline__ Vec<V> ld_stream(const float* p);
+
+template <>
+__device__ __forceinline__ Vec<1> ld_stream<1>(const float* p) {
+    Vec<1> r;
+    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r.v[0]) : "l"(p));
+    return r;
+}
+template <>
+__device__ __forceinline__ Vec<2> ld_stream<2>(const float* p) {
+    Vec<2> r;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0,%1}, [%2];" : "=f"(r.v[0]), "=f"(r.v[1]) : "l"(p));
+    return r;
+}
+template <>
+__device__ __forceinline__ Vec<4> ld_stream<4>(const float* p) {
+    Vec<4> r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3])
+                 : "l"(p));
+    return r;
+}
+template <>
+__device__ __forceinline__ Vec<8> ld_stream<8>(const float* p) {
+    Vec<8> r;
+    asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]),
+                   "=f"(r.v[4]), "=f"(r.v[5]), "=f"(r.v[6]), "=f"(r.v[7])
+                 : "l"(p));
+    return r;
+}
+
+template <int V>
+__device__ __forceinline__ void st_stream(float* p, const Vec<V>& r);
+
+template <>
+__device__ __forceinline__ void st_stream<1>(float* p, const Vec<1>& r) {
+    asm volatile("st.global.L1::no_allocate.f32 [%0], %1;" ::"l"(p), "f"(r.v[0]) : "memory");
+}
+template <>
+__device__ __forceinline__ void st_stream<2>(float* p, const Vec<2>& r) {
+    asm volatile("st.global.L1::no_allocate.v2.f32 [%0], {%1,%2};" ::"l"(p), "f"(r.v[0]), "f"(r.v[1]) : "memory");
+}
+template <>
+__device__ __forceinline__ void st_stream<4>(float* p, const Vec<4>& r) {
+    asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p),
+                 "f"(r.v[0]), "f"(r.v[1]), "f"(r.v[2]), "f"(r.v[3])
+                 : "memory");
+}
+template <>
+__device__ __forceinline__ void st_stream<8>(float* p, const Vec<8>& r) {
+    asm volatile("st.global.L1::no_allocate.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p),
+                 "f"(r.v[0]), "f"(r.v[1]), "f"(r.v[2]), "f"(r.v[3]), "f"(r.v[4]),
+                 "f"(r.v[5]), "f"(r.v[6]), "f"(r.v[7])
+                 : "memory");
+}
+
+// ------------------------------------------- programmatic dependent launch --
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// ------------------------------------------ TMA bulk copy into shared memory --
+// One elected thread arms an mbarrier with the expected byte count and issues
+// cp.async.bulk (global -> shared, SASS UBLKCP); every thread waits on the
+// barrier's phase 0.  `bytes` must be a multiple of 16, both addresses 16-byte
+// aligned.
+__device__ __forceinline__ void bulk_load_shared(void* smem_dst, const void* gmem_src, uint32_t bytes,
+                                                 uint64_t* bar) {
+    const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(d), "l"(gmem_src), "r"(bytes), "r"(b)
+                     : "memory");
+    }
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(b)
+            : "memory");
+    }
+}
+
+// ------------------------------------------------------------ one sample --
+// fp32 sample; returns the conditioning flag (always false for Heitz).
+template <int METHOD, bool PDF>
+__device__ __forceinline__ bool sample_one(float wx, float wy, float wz, float ax, float ay, float u1,
+                                           float u2, Sample& o) {
+    const float v1 = u1 - 0.5f;  // exact for u1 on the 2^-24 grid and for u1 >= 1/4
+    if (METHOD == kCap) return cap_fp32<PDF>(wx, wy, wz, ax, ay, v1, u2, 1.0f - u2, o);
+    if (METHOD == kCapNative) return cap_fp32<PDF, kFrameNative>(wx, wy, wz, ax, ay, v1, u2, 1.0f - u2, o);
+    heitz_fp32<PDF>(wx, wy, wz, ax, ay, v1, u2, o);
+    return false;
+}
+
+__device__ __forceinline__ void fix_one(const StreamArgs& a, bool pdf, int64_t i, bool flip) {
+    cap_fix_stream(a.wx, a.wy, a.wz, a.ax, a.ay, a.u1, a.u2, a.hx, a.hy, a.hz, pdf ? a.pdf : nullptr, i, flip);
+}

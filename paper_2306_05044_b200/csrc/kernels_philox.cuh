@@ -1,0 +1,168 @@
+// kernels_philox.cuh -- fused Philox4x32-10 kernels (config 4), the deferred fix-up queue
+// and kernel, raw Philox words, fix-up counters.
+// Part of libvndf's single translation unit (included by vndf.cu inside its
+// anonymous namespace); see vndf.cu for the kernel list and DESIGN.md s.6.
+#pragma once
+
+// ----------------------------------------------------- fused Philox kernel --
+// Deferred float64 fix-up queue of the fused kernel (compute-bound: inline
+// fp64 work would diverge the warp and its call would inflate the register
+// allocation).  Flagged local indices are appended with one (warp-aggregated)
+// atomic each (~0.4% of samples); a second kernel recomputes them with all
+// lanes busy.  If the queue overflowed (count > cap), the fix-up kernel
+// rescans every sample's flag instead: always correct, slower only then.
+struct FixQueue {
+    unsigned long long* count;
+    uint64_t* idx;
+    uint64_t cap;
+};
+
+template <int METHOD, bool PDF>
+__device__ __forceinline__ Sample philox_one(uint64_t seed, uint64_t first, uint64_t k,
+                                             const FixQueue& fq, const float2* __restrict__ tab) {
+    const Inputs in = c4_inputs_fp32(philox_sample(seed, first + k), tab);
+    Sample o;
+    if (METHOD == kCap) {
+        // config-4 inputs are on the upper hemisphere (wi.z = 1 - u > 0): no flip
+        const bool flag = cap_fp32<PDF, kFrameUpper>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o);
+        if (__builtin_expect(flag, 0)) {
+            const unsigned long long slot = atomicAdd(fq.count, 1ull);
+            if (slot < fq.cap) fq.idx[slot] = k;
+        }
+    } else {
+        heitz_fp32<PDF, false>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, o);
+    }
+    return o;
+}
+
+__global__ void __launch_bounds__(128) philox_fixup_kernel(uint64_t seed, uint64_t first, int64_t n,
+                                                            FixQueue fq, const float2* __restrict__ gtab,
+                                                            float* __restrict__ hx,
+                                                            float* __restrict__ hy, float* __restrict__ hz,
+                                                            float* __restrict__ pdf) {
+    const uint64_t count = *fq.count;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (count <= fq.cap) {
+        for (uint64_t t = t0; t < count; t += stride) {
+            const uint64_t k = fq.idx[t];
+            const float4 f = cap_philox_fp64(seed, first + k);
+            hx[k] = f.x;
+            hy[k] = f.y;
+            hz[k] = f.z;
+            if (pdf) pdf[k] = f.w;
+        }
+        return;
+    }
+    for (uint64_t k = t0; k < (uint64_t)n; k += stride) {  // overflow: rescan
+        const Inputs in = c4_inputs_fp32(philox_sample(seed, first + k), gtab);
+        Sample o;
+        if (cap_fp32<true, kFrameUpper>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o)) {
+            const float4 f = cap_philox_fp64(seed, first + k);
+            hx[k] = f.x;
+            hy[k] = f.y;
+            hz[k] = f.z;
+            if (pdf) pdf[k] = f.w;
+        }
+    }
+}
+
+#ifndef VNDF_PHILOX_MINB
+#define VNDF_PHILOX_MINB 1
+#endif
+#ifndef VNDF_PHILOX_V
+#define VNDF_PHILOX_V 4
+#endif
+
+template <int METHOD, bool PDF, int V>
+__global__ void __launch_bounds__(256, VNDF_PHILOX_MINB) philox_kernel(uint64_t seed, uint64_t first, int64_t n,
+                                                     float* __restrict__ hxp, float* __restrict__ hyp,
+                                                     float* __restrict__ hzp, float* __restrict__ pdfp,
+                                                     FixQueue fq, const float2* __restrict__ gtab) {
+    // Stage the 64 KB sin/cos table of the incidence azimuth in shared memory
+    // with one TMA bulk copy (cp.async.bulk, completion on an mbarrier).
+    extern __shared__ __align__(16) float2 tab[];
+    __shared__ __align__(8) uint64_t tab_bar;
+    bulk_load_shared(tab, gtab, kSinCosTableEntries * sizeof(float2), &tab_bar);
+    const int64_t nchunks = n / V;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int64_t c = tid; c < nchunks; c += stride) {
+        const int64_t i = c * V;
+        Vec<V> hx, hy, hz, pd;
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            const Sample o = philox_one<METHOD, PDF>(seed, first, (uint64_t)(i + j), fq, tab);
+            hx.v[j] = o.x;
+            hy.v[j] = o.y;
+            hz.v[j] = o.z;
+            pd.v[j] = o.pdf;
+        }
+        st_stream<V>(hxp + i, hx);
+        st_stream<V>(hyp + i, hy);
+        st_stream<V>(hzp + i, hz);
+        if (PDF) st_stream<V>(pdfp + i, pd);
+    }
+    if (V > 1) {
+        const int64_t i = nchunks * V + tid;
+        if (i < n) {
+            const Sample o = philox_one<METHOD, PDF>(seed, first, (uint64_t)i, fq, tab);
+            hxp[i] = o.x;
+            hyp[i] = o.y;
+            hzp[i] = o.z;
+            if (PDF) pdfp[i] = o.pdf;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) philox_words_kernel(uint64_t seed, uint64_t first, int64_t n,
+                                                           uint32_t block, uint4* __restrict__ out) {
+    const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+        const uint64_t i = first + (uint64_t)k;
+        out[k] = philox4x32_10(make_uint4((uint32_t)i, (uint32_t)(i >> 32), block, 0u), key);
+    }
+}
+
+// ------------------------------------------------------------ diagnostics --
+__device__ __forceinline__ void warp_count(bool flag, unsigned long long* count) {
+    const unsigned m = __ballot_sync(0xffffffffu, flag);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(count, (unsigned long long)__popc(m));
+}
+
+__global__ void __launch_bounds__(256) count_stream_kernel(StreamArgs a, int64_t n,
+                                                           unsigned long long* count) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t start = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t rounds = (n + stride - 1) / stride;  // uniform trip count for the ballot
+    for (int64_t r = 0; r < rounds; ++r) {
+        const int64_t i = start + r * stride;
+        bool flag = false;
+        if (i < n) {
+            Sample o;
+            const float u2 = a.u2[i];
+            flag = cap_fp32<true>(a.wx[i], a.wy[i], a.wz[i], a.ax[i], a.ay[i], a.u1[i] - 0.5f, u2,
+                                  1.0f - u2, o);
+        }
+        warp_count(flag, count);
+    }
+}
+
+__global__ void __launch_bounds__(256) count_philox_kernel(uint64_t seed, uint64_t first, int64_t n,
+                                                           const float2* __restrict__ gtab,
+                                                           unsigned long long* count) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t start = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t rounds = (n + stride - 1) / stride;
+    for (int64_t r = 0; r < rounds; ++r) {
+        const int64_t i = start + r * stride;
+        bool flag = false;
+        if (i < n) {
+            const Inputs in = c4_inputs_fp32(philox_sample(seed, first + (uint64_t)i), gtab);
+            Sample o;
+            flag = cap_fp32<true, kFrameUpper>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o);
+        }
+        warp_count(flag, count);
+    }
+}

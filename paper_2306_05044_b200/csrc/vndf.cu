@@ -1,19 +1,25 @@
-// vndf.cu -- libvndf: sm_100a kernels and the C ABI declared in include/vndf.h.
+// vndf.cu -- libvndf: host side and C ABI (include/vndf.h) of the sm_100a kernels.
 //
 // Citations: "P:n" = PAPER.md line n (arXiv 2306.05044).
 // describes each kernel, its roofline and its algorithmic bytes per sample.
 //
-// Kernels
-//   stream_kernel<METHOD, PDF, V>   streamed SoA sampling (cap or Heitz), V
-//                                   samples per thread per step loaded with
-//                                   one V*32-bit vector load per plane
-//                                   (V = 8: LDG.E.256 / STG.E.256 on sm_100a),
-//                                   persistent grid-stride loop, inline float64
-//                                   fix-up of flagged cap samples.
-//   philox_kernel<METHOD, PDF, V>   fused Philox4x32-10 input generation +
-//                                   sampling + pdf, stores only.
-//   philox_words_kernel             raw Philox words (bit-exactness audit).
-//   count_*_kernel                  diagnostics: how many samples get fixed up.
+// One translation unit:
+//   vndf_device.cuh      per-sample arithmetic (cap, Heitz, fp64 fix-ups, Philox,
+//                        config-4 generation, reflection, pdf)
+//   kernels_common.cuh   argument structs, 128/256-bit streaming loads and
+//                        stores, programmatic dependent launch, TMA bulk copy
+//   kernels_stream.cuh   stream_kernel<METHOD, PDF, V>: streamed SoA sampling
+//                        (cap, Heitz, native cap), one V-sample chunk per
+//                        thread, block-level float64 fix-up queue
+//   kernels_philox.cuh   philox_kernel<METHOD, PDF, V>: fused Philox4x32-10
+//                        generation + sampling + pdf, deferred fix-up queue and
+//                        kernel; raw Philox words; fix-up counters
+//   kernels_next.cuh     pdf_kernel (NEXT-4), reflect_kernel / furnace_kernel
+//                        (NEXT-2), histogram_kernel (NEXT-3), microbench_kernel
+//                        (NEXT-1)
+//   vndf.cu (this file)  launch configuration, argument validation, device
+//                        caches (occupancy, sin/cos table, memory pool, host
+//                        staging), the extern "C" entry points
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -34,696 +40,10 @@ using namespace vndf;
 
 namespace {
 
-// kCapNative: the paper's native below-horizon handling (NEXT-3, no flip)
-enum Method { kCap = 0, kHeitz = 1, kCapNative = 2 };
-
-struct StreamArgs {
-    const float* wx;
-    const float* wy;
-    const float* wz;
-    const float* ax;
-    const float* ay;
-    const float* u1;
-    const float* u2;
-    float* hx;
-    float* hy;
-    float* hz;
-    float* pdf;
-};
-
-// ---------------------------------------------------------------- memory ops
-// Streaming loads: read-only path, no L1 allocation (each byte is read once).
-template <int V>
-struct Vec {
-    float v[V];
-};
-
-template <int V>
-__device__ __forceinline__ Vec<V> ld_stream(const float* p);
-
-template <>
-__device__ __forceinline__ Vec<1> ld_stream<1>(const float* p) {
-    Vec<1> r;
-    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r.v[0]) : "l"(p));
-    return r;
-}
-template <>
-__device__ __forceinline__ Vec<2> ld_stream<2>(const float* p) {
-    Vec<2> r;
-    asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0,%1}, [%2];" : "=f"(r.v[0]), "=f"(r.v[1]) : "l"(p));
-    return r;
-}
-template <>
-__device__ __forceinline__ Vec<4> ld_stream<4>(const float* p) {
-    Vec<4> r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-                 : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3])
-                 : "l"(p));
-    return r;
-}
-template <>
-__device__ __forceinline__ Vec<8> ld_stream<8>(const float* p) {
-    Vec<8> r;
-    asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]),
-                   "=f"(r.v[4]), "=f"(r.v[5]), "=f"(r.v[6]), "=f"(r.v[7])
-                 : "l"(p));
-    return r;
-}
-
-template <int V>
-__device__ __forceinline__ void st_stream(float* p, const Vec<V>& r);
-
-template <>
-__device__ __forceinline__ void st_stream<1>(float* p, const Vec<1>& r) {
-    asm volatile("st.global.L1::no_allocate.f32 [%0], %1;" ::"l"(p), "f"(r.v[0]) : "memory");
-}
-template <>
-__device__ __forceinline__ void st_stream<2>(float* p, const Vec<2>& r) {
-    asm volatile("st.global.L1::no_allocate.v2.f32 [%0], {%1,%2};" ::"l"(p), "f"(r.v[0]), "f"(r.v[1]) : "memory");
-}
-template <>
-__device__ __forceinline__ void st_stream<4>(float* p, const Vec<4>& r) {
-    asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p),
-                 "f"(r.v[0]), "f"(r.v[1]), "f"(r.v[2]), "f"(r.v[3])
-                 : "memory");
-}
-template <>
-__device__ __forceinline__ void st_stream<8>(float* p, const Vec<8>& r) {
-    asm volatile("st.global.L1::no_allocate.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p),
-                 "f"(r.v[0]), "f"(r.v[1]), "f"(r.v[2]), "f"(r.v[3]), "f"(r.v[4]),
-                 "f"(r.v[5]), "f"(r.v[6]), "f"(r.v[7])
-                 : "memory");
-}
-
-// ------------------------------------------- programmatic dependent launch --
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_launch_dependents() {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
-
-// ------------------------------------------ TMA bulk copy into shared memory --
-// One elected thread arms an mbarrier with the expected byte count and issues
-// cp.async.bulk (global -> shared, SASS UBLKCP); every thread waits on the
-// barrier's phase 0.  `bytes` must be a multiple of 16, both addresses 16-byte
-// aligned.
-__device__ __forceinline__ void bulk_load_shared(void* smem_dst, const void* gmem_src, uint32_t bytes,
-                                                 uint64_t* bar) {
-    const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
-    const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
-    if (threadIdx.x == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                     ::"r"(d), "l"(gmem_src), "r"(bytes), "r"(b)
-                     : "memory");
-    }
-    uint32_t done = 0;
-    while (!done) {
-        asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}\n"
-            : "=r"(done)
-            : "r"(b)
-            : "memory");
-    }
-}
-
-// ------------------------------------------------------------ one sample --
-// fp32 sample; returns the conditioning flag (always false for Heitz).
-template <int METHOD, bool PDF>
-__device__ __forceinline__ bool sample_one(float wx, float wy, float wz, float ax, float ay, float u1,
-                                           float u2, Sample& o) {
-    const float v1 = u1 - 0.5f;  // exact for u1 on the 2^-24 grid and for u1 >= 1/4
-    if (METHOD == kCap) return cap_fp32<PDF>(wx, wy, wz, ax, ay, v1, u2, 1.0f - u2, o);
-    if (METHOD == kCapNative) return cap_fp32<PDF, kFrameNative>(wx, wy, wz, ax, ay, v1, u2, 1.0f - u2, o);
-    heitz_fp32<PDF>(wx, wy, wz, ax, ay, v1, u2, o);
-    return false;
-}
-
-__device__ __forceinline__ void fix_one(const StreamArgs& a, bool pdf, int64_t i, bool flip) {
-    cap_fix_stream(a.wx, a.wy, a.wz, a.ax, a.ay, a.u1, a.u2, a.hx, a.hy, a.hz, pdf ? a.pdf : nullptr, i, flip);
-}
-
-// ------------------------------------------------------- streamed kernel --
-// Chunk c covers samples [c V, c V + V).  Full chunks go through the vector
-// path (one chunk per thread by default, grid-stride if the grid is capped);
-// the n mod V tail is done by the first threads of the grid with scalar
-// accesses.  Flagged samples are pushed to a block-level shared-memory queue
-// and recomputed in float64 after a block barrier, one per thread, so a
-// block's few fix-ups (~3.5 per 1024 samples in config 5) run side by side
-// instead of serialising their warps; the vector loop itself stays call-free.
-// A queue overflow (only possible with a capped, grid-stride grid) falls back
-// to fixing in the thread that found it.
-constexpr int kBlockFixCap = 512;
-
-#ifndef VNDF_STREAM_MINB
-#define VNDF_STREAM_MINB 1
-#endif
-
-template <int METHOD, bool PDF, int V>
-__global__ void __launch_bounds__(256, VNDF_STREAM_MINB) stream_kernel(StreamArgs a, int64_t n) {
-    __shared__ int64_t fix_idx[METHOD != kHeitz ? kBlockFixCap : 1];
-    __shared__ int fix_count;
-    if (METHOD != kHeitz && threadIdx.x == 0) fix_count = 0;
-    // Programmatic dependent launch: let the next kernel on the stream be
-    // scheduled once every block of this grid is running, and wait for the
-    // previous grid (its completion and memory flush) before touching memory.
-    pdl_launch_dependents();
-    pdl_wait();
-    if (METHOD != kHeitz) __syncthreads();
-    auto defer = [&](int64_t i) {
-        const int slot = atomicAdd(&fix_count, 1);
-        if (slot < kBlockFixCap) fix_idx[slot] = i;
-        else fix_one(a, PDF, i, METHOD == kCap);
-    };
-    const int64_t nchunks = n / V;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    for (int64_t c = tid; c < nchunks; c += stride) {
-        const int64_t i = c * V;
-        const Vec<V> wx = ld_stream<V>(a.wx + i), wy = ld_stream<V>(a.wy + i),
-                     wz = ld_stream<V>(a.wz + i), ax = ld_stream<V>(a.ax + i),
-                     ay = ld_stream<V>(a.ay + i), u1 = ld_stream<V>(a.u1 + i),
-                     u2 = ld_stream<V>(a.u2 + i);
-        Vec<V> hx, hy, hz, pd;
-        unsigned flags = 0;
-#pragma unroll
-        for (int j = 0; j < V; ++j) {
-            Sample o;
-            const bool f = sample_one<METHOD, PDF>(wx.v[j], wy.v[j], wz.v[j], ax.v[j], ay.v[j],
-                                                   u1.v[j], u2.v[j], o);
-            flags |= (unsigned)f << j;
-            hx.v[j] = o.x;
-            hy.v[j] = o.y;
-            hz.v[j] = o.z;
-            pd.v[j] = o.pdf;
-        }
-        st_stream<V>(a.hx + i, hx);
-        st_stream<V>(a.hy + i, hy);
-        st_stream<V>(a.hz + i, hz);
-        if (PDF) st_stream<V>(a.pdf + i, pd);
-        if (METHOD != kHeitz && __builtin_expect(flags != 0, 0)) {
-            do {
-                const int j = __ffs(flags) - 1;
-                flags &= flags - 1;
-                defer(i + j);
-            } while (flags);
-        }
-    }
-    if (V > 1) {
-        const int64_t i = nchunks * V + tid;
-        if (i < n) {
-            Sample o;
-            const bool f = sample_one<METHOD, PDF>(a.wx[i], a.wy[i], a.wz[i], a.ax[i], a.ay[i],
-                                                   a.u1[i], a.u2[i], o);
-            a.hx[i] = o.x;
-            a.hy[i] = o.y;
-            a.hz[i] = o.z;
-            if (PDF) a.pdf[i] = o.pdf;
-            if (METHOD != kHeitz && f) defer(i);
-        }
-    }
-    if (METHOD != kHeitz) {
-        __syncthreads();
-        const int m = min(fix_count, kBlockFixCap);
-        for (int t = threadIdx.x; t < m; t += blockDim.x) fix_one(a, PDF, fix_idx[t], METHOD == kCap);
-    }
-}
-
-// ----------------------------------------------------- fused Philox kernel --
-// Deferred float64 fix-up queue of the fused kernel (compute-bound: inline
-// fp64 work would diverge the warp and its call would inflate the register
-// allocation).  Flagged local indices are appended with one (warp-aggregated)
-// atomic each (~0.4% of samples); a second kernel recomputes them with all
-// lanes busy.  If the queue overflowed (count > cap), the fix-up kernel
-// rescans every sample's flag instead: always correct, slower only then.
-struct FixQueue {
-    unsigned long long* count;
-    uint64_t* idx;
-    uint64_t cap;
-};
-
-template <int METHOD, bool PDF>
-__device__ __forceinline__ Sample philox_one(uint64_t seed, uint64_t first, uint64_t k,
-                                             const FixQueue& fq, const float2* __restrict__ tab) {
-    const Inputs in = c4_inputs_fp32(philox_sample(seed, first + k), tab);
-    Sample o;
-    if (METHOD == kCap) {
-        // config-4 inputs are on the upper hemisphere (wi.z = 1 - u > 0): no flip
-        const bool flag = cap_fp32<PDF, kFrameUpper>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o);
-        if (__builtin_expect(flag, 0)) {
-            const unsigned long long slot = atomicAdd(fq.count, 1ull);
-            if (slot < fq.cap) fq.idx[slot] = k;
-        }
-    } else {
-        heitz_fp32<PDF, false>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, o);
-    }
-    return o;
-}
-
-__global__ void __launch_bounds__(128) philox_fixup_kernel(uint64_t seed, uint64_t first, int64_t n,
-                                                            FixQueue fq, const float2* __restrict__ gtab,
-                                                            float* __restrict__ hx,
-                                                            float* __restrict__ hy, float* __restrict__ hz,
-                                                            float* __restrict__ pdf) {
-    const uint64_t count = *fq.count;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (count <= fq.cap) {
-        for (uint64_t t = t0; t < count; t += stride) {
-            const uint64_t k = fq.idx[t];
-            const float4 f = cap_philox_fp64(seed, first + k);
-            hx[k] = f.x;
-            hy[k] = f.y;
-            hz[k] = f.z;
-            if (pdf) pdf[k] = f.w;
-        }
-        return;
-    }
-    for (uint64_t k = t0; k < (uint64_t)n; k += stride) {  // overflow: rescan
-        const Inputs in = c4_inputs_fp32(philox_sample(seed, first + k), gtab);
-        Sample o;
-        if (cap_fp32<true, kFrameUpper>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o)) {
-            const float4 f = cap_philox_fp64(seed, first + k);
-            hx[k] = f.x;
-            hy[k] = f.y;
-            hz[k] = f.z;
-            if (pdf) pdf[k] = f.w;
-        }
-    }
-}
-
-#ifndef VNDF_PHILOX_MINB
-#define VNDF_PHILOX_MINB 1
-#endif
-#ifndef VNDF_PHILOX_V
-#define VNDF_PHILOX_V 4
-#endif
-
-template <int METHOD, bool PDF, int V>
-__global__ void __launch_bounds__(256, VNDF_PHILOX_MINB) philox_kernel(uint64_t seed, uint64_t first, int64_t n,
-                                                     float* __restrict__ hxp, float* __restrict__ hyp,
-                                                     float* __restrict__ hzp, float* __restrict__ pdfp,
-                                                     FixQueue fq, const float2* __restrict__ gtab) {
-    // Stage the 64 KB sin/cos table of the incidence azimuth in shared memory
-    // with one TMA bulk copy (cp.async.bulk, completion on an mbarrier).
-    extern __shared__ __align__(16) float2 tab[];
-    __shared__ __align__(8) uint64_t tab_bar;
-    bulk_load_shared(tab, gtab, kSinCosTableEntries * sizeof(float2), &tab_bar);
-    const int64_t nchunks = n / V;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    for (int64_t c = tid; c < nchunks; c += stride) {
-        const int64_t i = c * V;
-        Vec<V> hx, hy, hz, pd;
-#pragma unroll
-        for (int j = 0; j < V; ++j) {
-            const Sample o = philox_one<METHOD, PDF>(seed, first, (uint64_t)(i + j), fq, tab);
-            hx.v[j] = o.x;
-            hy.v[j] = o.y;
-            hz.v[j] = o.z;
-            pd.v[j] = o.pdf;
-        }
-        st_stream<V>(hxp + i, hx);
-        st_stream<V>(hyp + i, hy);
-        st_stream<V>(hzp + i, hz);
-        if (PDF) st_stream<V>(pdfp + i, pd);
-    }
-    if (V > 1) {
-        const int64_t i = nchunks * V + tid;
-        if (i < n) {
-            const Sample o = philox_one<METHOD, PDF>(seed, first, (uint64_t)i, fq, tab);
-            hxp[i] = o.x;
-            hyp[i] = o.y;
-            hzp[i] = o.z;
-            if (PDF) pdfp[i] = o.pdf;
-        }
-    }
-}
-
-__global__ void __launch_bounds__(256) philox_words_kernel(uint64_t seed, uint64_t first, int64_t n,
-                                                           uint32_t block, uint4* __restrict__ out) {
-    const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
-        const uint64_t i = first + (uint64_t)k;
-        out[k] = philox4x32_10(make_uint4((uint32_t)i, (uint32_t)(i >> 32), block, 0u), key);
-    }
-}
-
-// ------------------------------------------------------------ diagnostics --
-__device__ __forceinline__ void warp_count(bool flag, unsigned long long* count) {
-    const unsigned m = __ballot_sync(0xffffffffu, flag);
-    if ((threadIdx.x & 31) == 0 && m) atomicAdd(count, (unsigned long long)__popc(m));
-}
-
-__global__ void __launch_bounds__(256) count_stream_kernel(StreamArgs a, int64_t n,
-                                                           unsigned long long* count) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t start = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t rounds = (n + stride - 1) / stride;  // uniform trip count for the ballot
-    for (int64_t r = 0; r < rounds; ++r) {
-        const int64_t i = start + r * stride;
-        bool flag = false;
-        if (i < n) {
-            Sample o;
-            const float u2 = a.u2[i];
-            flag = cap_fp32<true>(a.wx[i], a.wy[i], a.wz[i], a.ax[i], a.ay[i], a.u1[i] - 0.5f, u2,
-                                  1.0f - u2, o);
-        }
-        warp_count(flag, count);
-    }
-}
-
-__global__ void __launch_bounds__(256) count_philox_kernel(uint64_t seed, uint64_t first, int64_t n,
-                                                           const float2* __restrict__ gtab,
-                                                           unsigned long long* count) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t start = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t rounds = (n + stride - 1) / stride;
-    for (int64_t r = 0; r < rounds; ++r) {
-        const int64_t i = start + r * stride;
-        bool flag = false;
-        if (i < n) {
-            const Inputs in = c4_inputs_fp32(philox_sample(seed, first + (uint64_t)i), gtab);
-            Sample o;
-            flag = cap_fp32<true, kFrameUpper>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o);
-        }
-        warp_count(flag, count);
-    }
-}
-
-// ------------------------------------------------- NEXT-4: standalone pdf --
-struct PdfArgs {
-    const float* hx;
-    const float* hy;
-    const float* hz;
-    const float* wx;
-    const float* wy;
-    const float* wz;
-    const float* ax;
-    const float* ay;
-    float* pdf;
-};
-
-// 32 B in (h, wi, alpha), 4 B out per sample; HBM-bound.
-template <int V>
-__global__ void __launch_bounds__(256) pdf_kernel(PdfArgs a, int64_t n) {
-    pdl_launch_dependents();
-    pdl_wait();
-    const int64_t nchunks = n / V;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    for (int64_t c = tid; c < nchunks; c += stride) {
-        const int64_t i = c * V;
-        const Vec<V> hx = ld_stream<V>(a.hx + i), hy = ld_stream<V>(a.hy + i), hz = ld_stream<V>(a.hz + i),
-                     wx = ld_stream<V>(a.wx + i), wy = ld_stream<V>(a.wy + i), wz = ld_stream<V>(a.wz + i),
-                     ax = ld_stream<V>(a.ax + i), ay = ld_stream<V>(a.ay + i);
-        Vec<V> pd;
-#pragma unroll
-        for (int j = 0; j < V; ++j)
-            pd.v[j] = vndf_pdf_fp32(hx.v[j], hy.v[j], hz.v[j], wx.v[j], wy.v[j], wz.v[j], ax.v[j], ay.v[j]);
-        st_stream<V>(a.pdf + i, pd);
-    }
-    if (V > 1) {
-        const int64_t i = nchunks * V + tid;
-        if (i < n) a.pdf[i] = vndf_pdf_fp32(a.hx[i], a.hy[i], a.hz[i], a.wx[i], a.wy[i], a.wz[i], a.ax[i], a.ay[i]);
-    }
-}
-
-// ------------------------------------------ NEXT-2: reflection sampling --
-struct ReflectArgs {
-    const float* wx;
-    const float* wy;
-    const float* wz;
-    const float* ax;
-    const float* ay;
-    const float* u1;
-    const float* u2;
-    float* ox;
-    float* oy;
-    float* oz;
-    float* pdf;
-    float* weight;
-};
-
-// Streamed: 28 B in, 20 B out per sample (wo.xyz, pdf Eq. 20, weight G2/G1).
-template <int V>
-__global__ void __launch_bounds__(256) reflect_kernel(ReflectArgs a, int64_t n) {
-    pdl_launch_dependents();
-    pdl_wait();
-    const int64_t nchunks = n / V;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    for (int64_t c = tid; c < nchunks; c += stride) {
-        const int64_t i = c * V;
-        const Vec<V> wx = ld_stream<V>(a.wx + i), wy = ld_stream<V>(a.wy + i),
-                     wz = ld_stream<V>(a.wz + i), ax = ld_stream<V>(a.ax + i),
-                     ay = ld_stream<V>(a.ay + i), u1 = ld_stream<V>(a.u1 + i),
-                     u2 = ld_stream<V>(a.u2 + i);
-        Vec<V> ox, oy, oz, pd, wt;
-        unsigned flags = 0;
-#pragma unroll
-        for (int j = 0; j < V; ++j) {
-            Reflected r;
-            const bool f = cap_reflect_fp32(wx.v[j], wy.v[j], wz.v[j], ax.v[j], ay.v[j], u1.v[j] - 0.5f,
-                                            u2.v[j], 1.0f - u2.v[j], r);
-            flags |= (unsigned)f << j;
-            ox.v[j] = r.x;
-            oy.v[j] = r.y;
-            oz.v[j] = r.z;
-            pd.v[j] = r.pdf;
-            wt.v[j] = r.weight;
-        }
-        st_stream<V>(a.ox + i, ox);
-        st_stream<V>(a.oy + i, oy);
-        st_stream<V>(a.oz + i, oz);
-        st_stream<V>(a.pdf + i, pd);
-        st_stream<V>(a.weight + i, wt);
-        while (__builtin_expect(flags != 0, 0)) {
-            const int j = __ffs(flags) - 1;
-            flags &= flags - 1;
-            cap_reflect_fix_stream(a.wx, a.wy, a.wz, a.ax, a.ay, a.u1, a.u2, a.ox, a.oy, a.oz, a.pdf,
-                                   a.weight, i + j);
-        }
-    }
-    if (V > 1) {
-        const int64_t i = nchunks * V + tid;
-        if (i < n) {
-            Reflected r;
-            const float u2 = a.u2[i];
-            const bool f = cap_reflect_fp32(a.wx[i], a.wy[i], a.wz[i], a.ax[i], a.ay[i], a.u1[i] - 0.5f, u2,
-                                            1.0f - u2, r);
-            a.ox[i] = r.x;
-            a.oy[i] = r.y;
-            a.oz[i] = r.z;
-            a.pdf[i] = r.pdf;
-            a.weight[i] = r.weight;
-            if (f)
-                cap_reflect_fix_stream(a.wx, a.wy, a.wz, a.ax, a.ay, a.u1, a.u2, a.ox, a.oy, a.oz, a.pdf,
-                                       a.weight, i);
-        }
-    }
-}
-
-// White-furnace estimator, Eq. 19 with L = 1: for a fixed (wa, alpha), sample j
-// (u1 = u(W0), u2 = u(W1) of Philox block (counter j, key seed)) contributes
-// its weight f_r |cos| / PDF = G2/G1.  Per-thread float64 sums, fixed-order
-// block reduction, per-block partials; a one-block pass adds the partials in
-// block order (deterministic for a given grid).
-template <int METHOD>
-__global__ void __launch_bounds__(256) furnace_kernel(float wx, float wy, float wz, float ax, float ay,
-                                                      uint64_t seed, uint64_t first, int64_t n,
-                                                      double* __restrict__ partials) {
-    double s1 = 0.0, s2 = 0.0;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
-        const uint4 W = philox_sample(seed, first + (uint64_t)j);
-        const float v1 = fmaf(fw(W.x), 0x1p-24f, -0.5f);
-        const float f2 = fw(W.y);
-        Reflected r;
-        if (METHOD == kCap) {
-            if (cap_reflect_fp32(wx, wy, wz, ax, ay, v1, f2 * 0x1p-24f, fmaf(f2, -0x1p-24f, 1.0f), r)) {
-                r.weight = cap_reflect_weight_fp64(wx, wy, wz, ax, ay, u01d(W.x), u01d(W.y));
-            }
-        } else {
-            heitz_reflect_fp32(wx, wy, wz, ax, ay, v1, f2 * 0x1p-24f, r);
-        }
-        s1 += r.weight;
-        s2 += (double)r.weight * r.weight;
-    }
-    __shared__ double sh1[8], sh2[8];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        s1 += __shfl_down_sync(0xffffffffu, s1, o);
-        s2 += __shfl_down_sync(0xffffffffu, s2, o);
-    }
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (lane == 0) {
-        sh1[warp] = s1;
-        sh2[warp] = s2;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double a1 = 0.0, a2 = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-            a1 += sh1[w];
-            a2 += sh2[w];
-        }
-        partials[2 * blockIdx.x] = a1;
-        partials[2 * blockIdx.x + 1] = a2;
-    }
-}
-
-__global__ void __launch_bounds__(256) furnace_finish_kernel(const double* __restrict__ partials, int blocks,
-                                                            double* out) {
-    // fixed-order reduction (deterministic for a given grid): strided partial
-    // sums per thread, then a shared-memory tree
-    __shared__ double r1[256], r2[256];
-    double a1 = 0.0, a2 = 0.0;
-    for (int b = threadIdx.x; b < blocks; b += blockDim.x) {
-        a1 += partials[2 * b];
-        a2 += partials[2 * b + 1];
-    }
-    r1[threadIdx.x] = a1;
-    r2[threadIdx.x] = a2;
-    __syncthreads();
-    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-        if ((int)threadIdx.x < w) {
-            r1[threadIdx.x] += r1[threadIdx.x + w];
-            r2[threadIdx.x] += r2[threadIdx.x + w];
-        }
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        out[0] = r1[0];
-        out[1] = r2[0];
-    }
-}
-
-// ------------------------------------ NEXT-3: GPU histograms for chi-square --
-// Samples a fixed (wi, alpha) n times (u1 = u(W0), u2 = u(W1) of Philox block
-// (counter j, key seed)) and bins, in shared memory, either
-//   mode 0: h in (theta in [0, pi/2), phi in [0, 2 pi))  (compare with Eq. 1 masses)
-//   mode 1: the std-space reflected direction c = reflect(ws, normalize(M^T h'))
-//           in (u_z = (c.z + ws.z)/(1 + ws.z), phi_c / 2 pi): uniform by Eq. 10.
-// METHOD: kCap / kHeitz (reading R4 frame) or kCapNative.  Cap samples flagged
-// by the conditioning test are recomputed in float64 first, as in the product
-// kernels.  Counts are ADDED to counts[nt * nphi] (uint64).
-template <int METHOD>
-__global__ void __launch_bounds__(256) histogram_kernel(int mode, float wx, float wy, float wz, float ax,
-                                                        float ay, uint64_t seed, uint64_t first, int64_t n,
-                                                        int nt, int nphi, unsigned long long* counts) {
-    extern __shared__ unsigned int bins[];
-    const int nb = nt * nphi;
-    for (int b = threadIdx.x; b < nb; b += blockDim.x) bins[b] = 0u;
-    __syncthreads();
-    const bool native = METHOD == kCapNative;
-    const float s = (!native && wz < 0.0f) ? -1.0f : 1.0f;
-    // std-space incidence (for mode 1)
-    const float tx = ax * wx, ty = ay * wy;
-    const float iL = s * rsqrtf(fmaf(tx, tx, fmaf(ty, ty, wz * wz)));
-    const float wsx = tx * iL, wsy = ty * iL, wsz = wz * iL;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
-        const uint4 W = philox_sample(seed, first + (uint64_t)j);
-        const float v1 = fmaf(fw(W.x), 0x1p-24f, -0.5f);
-        const float f2 = fw(W.y);
-        const float u2 = f2 * 0x1p-24f, q = fmaf(f2, -0x1p-24f, 1.0f);
-        Sample o;
-        if (METHOD == kHeitz) {
-            heitz_fp32<false>(wx, wy, wz, ax, ay, v1, u2, o);
-        } else {
-            const bool f = native ? cap_fp32<false, kFrameNative>(wx, wy, wz, ax, ay, v1, u2, q, o)
-                                  : cap_fp32<false>(wx, wy, wz, ax, ay, v1, u2, q, o);
-            if (f) {
-                const float4 d = cap_fp64(wx, wy, wz, ax, ay, fw(W.x) * 0x1p-24f, u2, !native);
-                o.x = d.x;
-                o.y = d.y;
-                o.z = d.z;
-            }
-        }
-        int ib;
-        if (mode == 0) {
-            const float th = acosf(fminf(fmaxf(o.z, -1.0f), 1.0f));
-            float ph = atan2f(o.y, o.x);
-            if (ph < 0.0f) ph += 6.28318530717958648f;
-            const int it = min(max((int)(th * (float)nt * 0.636619772367581343f), 0), nt - 1);
-            const int ip = min(max((int)(ph * (float)nphi * 0.159154943091895336f), 0), nphi - 1);
-            ib = it * nphi + ip;
-        } else {
-            // h' = s h (sampling frame), hs ~ M^T h'
-            float hx = s * o.x / ax, hy = s * o.y / ay, hz = s * o.z;
-            const float ih = rsqrtf(fmaf(hx, hx, fmaf(hy, hy, hz * hz)));
-            hx *= ih; hy *= ih; hz *= ih;
-            const float d = 2.0f * fmaf(hx, wsx, fmaf(hy, wsy, hz * wsz));
-            const float cx = fmaf(d, hx, -wsx), cy = fmaf(d, hy, -wsy), cz = fmaf(d, hz, -wsz);
-            const float uz = (cz + wsz) / (1.0f + wsz);
-            float ph = atan2f(cy, cx);
-            if (ph < 0.0f) ph += 6.28318530717958648f;
-            const int it = min(max((int)(uz * (float)nt), 0), nt - 1);
-            const int ip = min(max((int)(ph * (float)nphi * 0.159154943091895336f), 0), nphi - 1);
-            ib = it * nphi + ip;
-        }
-        atomicAdd(&bins[ib], 1u);
-    }
-    __syncthreads();
-    for (int b = threadIdx.x; b < nb; b += blockDim.x)
-        if (bins[b]) atomicAdd(&counts[b], (unsigned long long)bins[b]);
-}
-
-// ------------------------------------- NEXT-1: sampler-only microbenchmark --
-// The paper's GPU methodology: each lane calls Listing 1 `iters`
-// times.  Lane t draws its incidence and roughness once from the config-4
-// recipe (Philox block of index t).  Iteration k uses the integer Weyl
-// sequence u1 = u(s1 + k A1), u2 = u(s2 + k A2) (s1 = W0, s2 = W1) and then
-// rotates wi about z by a fixed angle with explicitly rounded fp32 operations
-// (so every call does the full Listing 1 -- nothing is loop-invariant -- and
-// the host oracle can replay the exact fp32 incidences).  h.x + 2 h.y + 3 h.z
-// is summed into a per-lane checksum (the sink).  No pdf, no flag, no fix-up.
-// VARIANT 0 = cap (production fp32 arithmetic), 1 = Heitz (Listing 2),
-// 2 = Listing 3 literal.
-constexpr uint32_t kWeyl1 = 0x9E3779B9u, kWeyl2 = 0x7F4A7C15u;
-constexpr float kRotC = 0.764842187f, kRotS = 0.644217687f;  // cos, sin of 0.7 rad (fp32)
-
-template <int VARIANT>
-__global__ void __launch_bounds__(256) microbench_kernel(uint64_t seed, int64_t lanes, int iters,
-                                                         const float2* __restrict__ gtab,
-                                                         float* __restrict__ checksum) {
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= lanes) return;
-    const uint4 W = philox_sample(seed, (uint64_t)t);
-    const Inputs in = c4_inputs_fp32(W, gtab);
-    uint32_t x1 = W.x, x2 = W.y;
-    float wx = in.wx, wy = in.wy;
-    float acc = 0.0f;
-#pragma unroll 4
-    for (int k = 0; k < iters; ++k) {
-        const float v1 = fmaf(fw(x1), 0x1p-24f, -0.5f);
-        const float f2 = fw(x2);
-        Sample o;
-        if (VARIANT == 0) {
-            cap_fp32<false, kFrameUpper>(wx, wy, in.wz, in.ax, in.ay, v1, f2 * 0x1p-24f,
-                                   fmaf(f2, -0x1p-24f, 1.0f), o);
-        } else if (VARIANT == 1) {
-            heitz_fp32<false, false>(wx, wy, in.wz, in.ax, in.ay, v1, f2 * 0x1p-24f, o);
-        } else {
-            cap_literal_fp32(wx, wy, in.wz, in.ax, in.ay, v1, f2 * 0x1p-24f, o);
-        }
-        acc += o.x + 2.0f * o.y + 3.0f * o.z;
-        x1 += kWeyl1;
-        x2 += kWeyl2;
-        const float rx = __fmaf_rn(kRotC, wx, -__fmul_rn(kRotS, wy));
-        const float ry = __fmaf_rn(kRotC, wy, __fmul_rn(kRotS, wx));
-        wx = rx;
-        wy = ry;
-    }
-    checksum[t] = acc;
-}
+#include "kernels_common.cuh"
+#include "kernels_stream.cuh"
+#include "kernels_philox.cuh"
+#include "kernels_next.cuh"
 
 // =============================================================== host side ==
 thread_local int g_last_cuda_error = 0;
