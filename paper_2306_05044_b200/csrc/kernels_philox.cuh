@@ -18,9 +18,9 @@ struct FixQueue {
 };
 
 template <int METHOD, bool PDF>
-__device__ __forceinline__ Sample philox_one(uint64_t seed, uint64_t first, uint64_t k,
+__device__ __forceinline__ Sample philox_one(const PhiloxKeys& ks, uint64_t first, uint64_t k,
                                              const FixQueue& fq, const float2* __restrict__ tab) {
-    const Inputs in = c4_inputs_fp32(philox_sample(seed, first + k), tab);
+    const Inputs in = c4_inputs_fp32(philox_sample_ks(ks, first + k), tab);
     Sample o;
     if (METHOD == kCap) {
         // config-4 inputs are on the upper hemisphere (wi.z = 1 - u > 0): no flip
@@ -78,7 +78,8 @@ template <int METHOD, bool PDF, int V>
 __global__ void __launch_bounds__(256, VNDF_PHILOX_MINB) philox_kernel(uint64_t seed, uint64_t first, int64_t n,
                                                      float* __restrict__ hxp, float* __restrict__ hyp,
                                                      float* __restrict__ hzp, float* __restrict__ pdfp,
-                                                     FixQueue fq, const float2* __restrict__ gtab) {
+                                                     FixQueue fq, const float2* __restrict__ gtab,
+                                                     const __grid_constant__ PhiloxKeys ks) {
     // Stage the 64 KB sin/cos table of the incidence azimuth in shared memory
     // with one TMA bulk copy (cp.async.bulk, completion on an mbarrier).
     extern __shared__ __align__(16) float2 tab[];
@@ -92,7 +93,7 @@ __global__ void __launch_bounds__(256, VNDF_PHILOX_MINB) philox_kernel(uint64_t 
         Vec<V> hx, hy, hz, pd;
 #pragma unroll
         for (int j = 0; j < V; ++j) {
-            const Sample o = philox_one<METHOD, PDF>(seed, first, (uint64_t)(i + j), fq, tab);
+            const Sample o = philox_one<METHOD, PDF>(ks, first, (uint64_t)(i + j), fq, tab);
             hx.v[j] = o.x;
             hy.v[j] = o.y;
             hz.v[j] = o.z;
@@ -106,7 +107,7 @@ __global__ void __launch_bounds__(256, VNDF_PHILOX_MINB) philox_kernel(uint64_t 
     if (V > 1) {
         const int64_t i = nchunks * V + tid;
         if (i < n) {
-            const Sample o = philox_one<METHOD, PDF>(seed, first, (uint64_t)i, fq, tab);
+            const Sample o = philox_one<METHOD, PDF>(ks, first, (uint64_t)i, fq, tab);
             hxp[i] = o.x;
             hyp[i] = o.y;
             hzp[i] = o.z;

@@ -346,7 +346,8 @@ vndf_status launch_philox_v(uint64_t seed, uint64_t first, int64_t n, float* hx,
         if (qbuf) cudaFreeAsync(qbuf, s);
         return cuda_fail(e);
     }
-    philox_kernel<METHOD, PDF, V><<<grid, block, smem, s>>>(seed, first, n, hx, hy, hz, pdf, fq, gtab);
+    philox_kernel<METHOD, PDF, V><<<grid, block, smem, s>>>(seed, first, n, hx, hy, hz, pdf, fq, gtab,
+                                                            philox_keys(seed));
     e = cudaGetLastError();
     if (e == cudaSuccess && METHOD == kCap) {
         // one thread per queue slot up to SMs x 32 blocks; blocks past the

@@ -479,6 +479,37 @@ __device__ __forceinline__ float fw16(uint32_t lo, uint32_t hi) {
     return __uint2float_rn(__byte_perm(lo, hi, 0x7740) & 0xFFFFu);
 }
 
+// The per-round Philox keys of a seed, precomputed on the host and passed as a
+// __grid_constant__ kernel parameter: the round XORs then read them from the
+// constant bank (LOP3 ... c[0x0][...]) instead of occupying 20 registers.
+struct PhiloxKeys {
+    uint32_t k0[10], k1[10];
+};
+
+inline PhiloxKeys philox_keys(uint64_t seed) {
+    PhiloxKeys ks;
+    uint32_t a = (uint32_t)seed, b = (uint32_t)(seed >> 32);
+    for (int r = 0; r < 10; ++r) {
+        ks.k0[r] = a;
+        ks.k1[r] = b;
+        a += 0x9E3779B9u;
+        b += 0xBB67AE85u;
+    }
+    return ks;
+}
+
+__device__ __forceinline__ uint4 philox_sample_ks(const PhiloxKeys& ks, uint64_t i) {
+    uint4 c = make_uint4((uint32_t)i, (uint32_t)(i >> 32), 0u, 0u);
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        uint32_t hi0, lo0, hi1, lo1;
+        mul_hilo(0xD2511F53u, c.x, hi0, lo0);
+        mul_hilo(0xCD9E8D57u, c.z, hi1, lo1);
+        c = make_uint4(hi1 ^ c.y ^ ks.k0[r], lo1, hi0 ^ c.w ^ ks.k1[r], lo0);
+    }
+    return c;
+}
+
 __device__ __forceinline__ uint4 philox_sample(uint64_t seed, uint64_t i) {
     return philox4x32_10(make_uint4((uint32_t)i, (uint32_t)(i >> 32), 0u, 0u),
                          make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
