@@ -8,6 +8,14 @@
 // kCapNative: the paper's native below-horizon handling (NEXT-3, no flip)
 enum Method { kCap = 0, kHeitz = 1, kCapNative = 2 };
 
+// A device queue of sample indices for deferred float64 fix-ups: a counter
+// and `cap` slots (library pool memory, one per call).
+struct FixQueue {
+    unsigned long long* count;
+    uint64_t* idx;
+    uint64_t cap;
+};
+
 struct StreamArgs {
     const float* wx;
     const float* wy;
@@ -24,6 +32,17 @@ struct StreamArgs {
 
 // ---------------------------------------------------------------- memory ops
 // Streaming loads: read-only path, no L1 allocation (each byte is read once).
+// L2 eviction priority of the 128/256-bit streaming accesses (measured on B200,
+// tools/stream_variants.py): inputs evict-last (the block-level fix-ups re-read
+// a few of them), outputs evict-first (written once, never re-read): +1.7% on
+// config 2, +5% on config 5 against the default evict-normal.
+#ifndef VNDF_LD_L2
+#define VNDF_LD_L2 ".L2::evict_last"
+#endif
+#ifndef VNDF_ST_L2
+#define VNDF_ST_L2 ".L2::evict_first"
+#endif
+
 template <int V>
 struct Vec {
     float v[V];
@@ -47,15 +66,16 @@ __device__ __forceinline__ Vec<2> ld_stream<2>(const float* p) {
 template <>
 __device__ __forceinline__ Vec<4> ld_stream<4>(const float* p) {
     Vec<4> r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+    asm volatile("ld.global.nc.L1::no_allocate" VNDF_LD_L2 ".v4.f32 {%0,%1,%2,%3}, [%4];"
                  : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3])
                  : "l"(p));
     return r;
 }
+
 template <>
 __device__ __forceinline__ Vec<8> ld_stream<8>(const float* p) {
     Vec<8> r;
-    asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+    asm volatile("ld.global.nc.L1::no_allocate" VNDF_LD_L2 ".v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]),
                    "=f"(r.v[4]), "=f"(r.v[5]), "=f"(r.v[6]), "=f"(r.v[7])
                  : "l"(p));
@@ -75,13 +95,13 @@ __device__ __forceinline__ void st_stream<2>(float* p, const Vec<2>& r) {
 }
 template <>
 __device__ __forceinline__ void st_stream<4>(float* p, const Vec<4>& r) {
-    asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p),
+    asm volatile("st.global.L1::no_allocate" VNDF_ST_L2 ".v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p),
                  "f"(r.v[0]), "f"(r.v[1]), "f"(r.v[2]), "f"(r.v[3])
                  : "memory");
 }
 template <>
 __device__ __forceinline__ void st_stream<8>(float* p, const Vec<8>& r) {
-    asm volatile("st.global.L1::no_allocate.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p),
+    asm volatile("st.global.L1::no_allocate" VNDF_ST_L2 ".v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p),
                  "f"(r.v[0]), "f"(r.v[1]), "f"(r.v[2]), "f"(r.v[3]), "f"(r.v[4]),
                  "f"(r.v[5]), "f"(r.v[6]), "f"(r.v[7])
                  : "memory");

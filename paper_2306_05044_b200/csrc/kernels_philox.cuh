@@ -11,11 +11,6 @@
 // atomic each (~0.4% of samples); a second kernel recomputes them with all
 // lanes busy.  If the queue overflowed (count > cap), the fix-up kernel
 // rescans every sample's flag instead: always correct, slower only then.
-struct FixQueue {
-    unsigned long long* count;
-    uint64_t* idx;
-    uint64_t cap;
-};
 
 template <int METHOD, bool PDF>
 __device__ __forceinline__ Sample philox_one(const PhiloxKeys& ks, uint64_t first, uint64_t k,
