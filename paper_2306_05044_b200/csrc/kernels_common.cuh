@@ -32,7 +32,8 @@ struct StreamArgs {
 
 // ---------------------------------------------------------------- memory ops
 // Streaming loads: read-only path, no L1 allocation (each byte is read once).
-// L2 eviction priority of the 128/256-bit streaming accesses (measured on B200,
+// L2 eviction priority of the 256-bit streaming accesses (PTX allows the
+// .L2::evict_* qualifiers on 256-bit accesses only) (measured on B200,
 // tools/stream_variants.py): inputs evict-last (the block-level fix-ups re-read
 // a few of them), outputs evict-first (written once, never re-read): +1.7% on
 // config 2, +5% on config 5 against the default evict-normal.
@@ -66,7 +67,7 @@ __device__ __forceinline__ Vec<2> ld_stream<2>(const float* p) {
 template <>
 __device__ __forceinline__ Vec<4> ld_stream<4>(const float* p) {
     Vec<4> r;
-    asm volatile("ld.global.nc.L1::no_allocate" VNDF_LD_L2 ".v4.f32 {%0,%1,%2,%3}, [%4];"
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
                  : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3])
                  : "l"(p));
     return r;
@@ -95,7 +96,7 @@ __device__ __forceinline__ void st_stream<2>(float* p, const Vec<2>& r) {
 }
 template <>
 __device__ __forceinline__ void st_stream<4>(float* p, const Vec<4>& r) {
-    asm volatile("st.global.L1::no_allocate" VNDF_ST_L2 ".v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p),
+    asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p),
                  "f"(r.v[0]), "f"(r.v[1]), "f"(r.v[2]), "f"(r.v[3])
                  : "memory");
 }
