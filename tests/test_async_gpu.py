@@ -26,7 +26,7 @@ def test_calls_do_not_synchronise(env):
     n = 1 << 30
     out = vndf.empty_outputs(n, dev)
     s = torch.cuda.Stream(dev)
-    vndf.vndf_sample_cap_philox(3, 0, 1 << 20, *out, stream=s)   # warm: table, pool, attributes
+    vndf.vndf_sample_cap_philox(3, 0, n, *out, stream=s)         # warm: table, pool growth, attributes
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     vndf.vndf_sample_cap_philox(3, 0, n, *out, stream=s)         # ~6 ms of GPU work
