@@ -91,3 +91,30 @@ def two_sample(c1: np.ndarray, c2: np.ndarray, min_expected: float = 5.0):
     chi2 = float((((A - EA) ** 2 / EA)[ok]).sum() + (((B - EB) ** 2 / EB)[ok]).sum())
     dof = int(ok.sum() - 1)
     return chi2, dof, float(_st.chi2.sf(chi2, dof))
+
+
+def sphere_bin_masses(pdf_dirs, nz: int = 32, nphi: int = 64, q: int = 12) -> np.ndarray:
+    """Masses of a density over the whole sphere in nz x nphi bins of
+    (z = cos theta uniform on [-1, 1], phi uniform on [0, 2 pi)), by q x q
+    Gauss-Legendre per bin (z is the uniform-area coordinate).  pdf_dirs maps a
+    (3, k) array of unit directions to k densities."""
+    x, w = np.polynomial.legendre.leggauss(q)
+    zb = np.linspace(-1.0, 1.0, nz + 1)
+    pb = np.linspace(0.0, 2 * np.pi, nphi + 1)
+    zz = (0.5 * (zb[1:] - zb[:-1]))[:, None] * x[None, :] + (0.5 * (zb[1:] + zb[:-1]))[:, None]
+    pp = (0.5 * (pb[1:] - pb[:-1]))[:, None] * x[None, :] + (0.5 * (pb[1:] + pb[:-1]))[:, None]
+    Z, P = np.meshgrid(zz.reshape(-1), pp.reshape(-1), indexing="ij")
+    r = np.sqrt(np.clip(1 - Z * Z, 0, None))
+    d = np.stack([r * np.cos(P), r * np.sin(P), Z]).reshape(3, -1)
+    f = pdf_dirs(d).reshape(nz, q, nphi, q)
+    return np.einsum("aibj,i,j->ab", f, 0.5 * (zb[1] - zb[0]) * w, 0.5 * (pb[1] - pb[0]) * w)
+
+
+def sphere_histogram(v: np.ndarray, nz: int = 32, nphi: int = 64) -> np.ndarray:
+    v = np.asarray(v, dtype=np.float64).reshape(3, -1)
+    v = v / np.linalg.norm(v, axis=0)
+    iz = np.clip(((v[2] + 1) * 0.5 * nz).astype(np.int64), 0, nz - 1)
+    ip = np.clip((np.mod(np.arctan2(v[1], v[0]), 2 * np.pi) / (2 * np.pi) * nphi).astype(np.int64), 0, nphi - 1)
+    out = np.zeros((nz, nphi), dtype=np.int64)
+    np.add.at(out, (iz, ip), 1)
+    return out

@@ -118,3 +118,22 @@ def test_furnace_estimator_converges_to_albedo(orc, theta, alpha):
         assert abs(v1 / v0 - 1) < 0.05
     if theta == 0 and alpha == (0.1, 0.1):
         assert m0 >= 0.95  # near-specular single-scatter albedo at normal incidence
+
+
+@pytest.mark.parametrize("method", [CAP, HEITZ], ids=["cap", "heitz"])
+@pytest.mark.parametrize("theta,alpha", [(30, (0.4, 0.4)), (70, (0.3, 0.6)), (0, (1.0, 1.0))])
+def test_reflected_directions_follow_eq20(orc, method, theta, alpha):
+    """The appendix's sampling steps (1)-(2) produce directions distributed as
+    Eq. 20 over the whole sphere (below-horizon reflections included)."""
+    from oracle import stats
+    wa = _dir(theta, 40)
+    n = 1 << 19
+    rng = np.random.default_rng(60 + method + theta)
+    u = rng.random((2, n), dtype=np.float32)
+    wa32 = wa.astype(np.float32)
+    out = orc.batch_sample_reflect(method, np.full(n, wa32[0]), np.full(n, wa32[1]), np.full(n, wa32[2]),
+                                   np.full(n, alpha[0], np.float32), np.full(n, alpha[1], np.float32), u[0], u[1])
+    masses = stats.sphere_bin_masses(lambda d: orc.batch_pdf_reflect(wa32.astype(np.float64), *alpha, d))
+    assert masses.sum() == pytest.approx(1.0, abs=2e-3)
+    _, _, pv = stats.pearson(stats.sphere_histogram(out[:3]), masses)
+    assert pv > 1e-3, pv

@@ -77,3 +77,24 @@ def test_furnace_gpu(env, method, theta, alpha):
     albedo = float((oracle.batch_brdf_cos(wa.astype(np.float64), *alpha, dirs) * w).sum())
     se = np.sqrt(max(var, 0) / n)
     assert abs(mean - albedo) <= 5 * se + 1e-5, (mean, albedo, se)
+
+
+@pytest.mark.parametrize("theta,alpha", [(30, (0.4, 0.4)), (70, (0.3, 0.6)), (85, (0.2, 0.2))])
+def test_reflect_gpu_distribution_eq20(env, theta, alpha):
+    """GPU reflected directions (2^21 per seed, 3 seeds) against the Eq. 20 masses
+    over the whole sphere (32 x 64 bins in (cos theta, phi))."""
+    oracle, vndf, synth, dev = env
+    from oracle import stats
+    t = np.radians(theta)
+    wa = np.array([np.sin(t) * np.cos(0.7), np.sin(t) * np.sin(0.7), np.cos(t)], dtype=np.float32)
+    masses = stats.sphere_bin_masses(lambda d: oracle.batch_pdf_reflect(wa.astype(np.float64), *alpha, d))
+    passes = []
+    for seed in (3000, 3001, 3002):
+        n = 1 << 21
+        x = synth.fill(0, seed, n, device=dev, fixed=[wa[0], wa[1], wa[2], alpha[0], alpha[1]])
+        out = [torch.empty(n, dtype=torch.float32, device=dev) for _ in range(5)]
+        vndf.vndf_sample_cap_reflect(*[x[k] for k in synth.PLANES], *out)
+        torch.cuda.synchronize()
+        wo = np.stack([o.cpu().numpy() for o in out[:3]]).astype(np.float64)
+        passes.append(stats.pearson(stats.sphere_histogram(wo), masses)[2] > 1e-3)
+    assert sum(passes) >= 2, passes
