@@ -41,8 +41,11 @@
  *   - Calls only ENQUEUE work on `stream` (NULL = legacy default stream) and
  *     return; outputs are valid once the caller synchronises the stream.
  *     The *_host call is the exception: it is blocking.
- *   - Thread-safe; the only global state is a per-device cache of device
- *     attributes and launch configurations.
+ *   - Thread-safe.  Global state, per device, created on first use and kept
+ *     for the life of the process: cached device attributes and launch
+ *     configurations, a 64 KB sin/cos table (fused Philox path), a private
+ *     stream-ordered memory pool for transient fix-up queues, and the host
+ *     entry point's staging area (see vndf_release_host_staging).
  *   - Outputs are a pure function of the inputs (of seed and global index for
  *     the Philox calls): independent of grid, stream, vector path or chunking.
  *
@@ -130,7 +133,8 @@ vndf_status vndf_sample_heitz2018_philox(uint64_t seed, uint64_t first_index, in
                                          vndf_stream_t stream);
 
 /* Raw Philox4x32-10 words of block `block` for global indices
- * first_index .. first_index + n - 1: words[4k .. 4k+3] (test / audit). */
+ * first_index .. first_index + n - 1: words[4k .. 4k+3] (test / audit).
+ * words: device pointer to 4n uint32, 16-byte aligned (one uint4 per index). */
 vndf_status vndf_philox4x32_10(uint64_t seed, uint64_t first_index, int64_t n,
                                uint32_t block, uint32_t *words, vndf_stream_t stream);
 
