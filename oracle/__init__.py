@@ -28,11 +28,23 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 CFLAGS = ["-O2", "-std=c11", "-fPIC", "-shared", "-pthread", "-ffp-contract=off"]
 
 
+def _stale() -> bool:
+    return not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC)
+
+
 def build(force: bool = False) -> str:
-    """Compile oracle.c into liboracle.so (gcc).  Returns the library path."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        cmd = ["gcc", *CFLAGS, _SRC, "-o", _LIB, "-lquadmath", "-lm"]
-        subprocess.run(cmd, check=True)
+    """Compile oracle.c into liboracle.so (gcc).  Returns the library path.
+    Concurrent callers (several processes) serialise on a lock file."""
+    import fcntl
+    if not (force or _stale()):
+        return _LIB
+    with open(_LIB + ".lock", "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        if force or _stale():
+            cmd = ["gcc", *CFLAGS, _SRC, "-o", _LIB + ".tmp", "-lquadmath", "-lm"]
+            subprocess.run(cmd, check=True)
+            os.replace(_LIB + ".tmp", _LIB)
+        fcntl.flock(lk, fcntl.LOCK_UN)
     return _LIB
 
 

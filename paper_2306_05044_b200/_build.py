@@ -34,7 +34,33 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in DEPS)
 
 
+class _FileLock:
+    """Exclusive advisory lock: concurrent builders (e.g. every torchrun rank
+    calling build()) compile once; the others wait and then see a fresh file."""
+
+    def __init__(self, path: str):
+        self.path = path
+
+    def __enter__(self):
+        import fcntl
+        self.f = open(self.path, "w")
+        fcntl.flock(self.f, fcntl.LOCK_EX)
+        return self
+
+    def __exit__(self, *exc):
+        import fcntl
+        fcntl.flock(self.f, fcntl.LOCK_UN)
+        self.f.close()
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    if not (force or stale()):
+        return LIB
+    with _FileLock(LIB + ".lock"):
+        return _build_locked(force, verbose)
+
+
+def _build_locked(force: bool, verbose: bool) -> str:
     if force or stale():
         cmd = [NVCC, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), *SOURCES, "-o", LIB + ".tmp"]
         res = subprocess.run(cmd, capture_output=True, text=True)

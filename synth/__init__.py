@@ -51,6 +51,14 @@ PLANES = ("wi_x", "wi_y", "wi_z", "alpha_x", "alpha_y", "u1", "u2")
 
 
 def build(force: bool = False) -> str:
+    from paper_2306_05044_b200._build import _FileLock  # build plumbing only (no method code)
+    if not (force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC)):
+        return LIB
+    with _FileLock(LIB + ".lock"):
+        return _build_locked(force)
+
+
+def _build_locked(force: bool) -> str:
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
         cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17",
                "-shared", "-Xcompiler", "-fPIC", "-cudart", "static", SRC, "-o", LIB + ".tmp"]
