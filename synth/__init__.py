@@ -51,11 +51,16 @@ PLANES = ("wi_x", "wi_y", "wi_z", "alpha_x", "alpha_y", "u1", "u2")
 
 
 def build(force: bool = False) -> str:
-    from paper_2306_05044_b200._build import _FileLock  # build plumbing only (no method code)
+    """nvcc sm_100a build of libvndf_synth.so; concurrent callers serialise on a lock file."""
+    import fcntl
     if not (force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC)):
         return LIB
-    with _FileLock(LIB + ".lock"):
-        return _build_locked(force)
+    with open(LIB + ".lock", "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        try:
+            return _build_locked(force)
+        finally:
+            fcntl.flock(lk, fcntl.LOCK_UN)
 
 
 def _build_locked(force: bool) -> str:
