@@ -62,8 +62,10 @@ __global__ void __launch_bounds__(128) philox_fixup_kernel(uint64_t seed, uint64
     }
 }
 
+// 3 resident 256-thread blocks per SM (<= 85 registers; 3 x 64 KB of staged
+// table fit the 228 KB of shared memory): +1% over the unconstrained build.
 #ifndef VNDF_PHILOX_MINB
-#define VNDF_PHILOX_MINB 1
+#define VNDF_PHILOX_MINB 3
 #endif
 #ifndef VNDF_PHILOX_V
 #define VNDF_PHILOX_V 4
