@@ -102,7 +102,7 @@ class ClockSampler:
 
     def __init__(self, index: int, period_s: float = 0.005):
         self.index, self.period = index, period_s
-        self.samples, self.reasons = [], set()
+        self.samples, self.reasons, self.power = [], set(), []
         self.max_mhz = None
         self._stop = threading.Event()
         self._nv = None
@@ -119,6 +119,10 @@ class ClockSampler:
         nv = self._nv
         try:
             self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+            try:
+                self.power.append(nv.nvmlDeviceGetPowerUsage(self._h) / 1000.0)
+            except Exception:
+                pass
             r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
             names = {nv.nvmlClocksEventReasonHwSlowdown: "hw_slowdown",
                      nv.nvmlClocksEventReasonHwThermalSlowdown: "hw_thermal_slowdown",
@@ -154,8 +158,11 @@ class ClockSampler:
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
         s = sorted(self.samples)
-        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                "n_samples": len(s)}
+        out = {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+               "n_samples": len(s)}
+        if self.power:
+            out["power_w_max"] = round(max(self.power), 1)
+        return out
 
 
 # ------------------------------------------------------------ timed loops ---
