@@ -93,3 +93,32 @@ def test_beyond_2e31_samples(env):
     assert np.abs(h - h_ref).max() <= TOL_H
     del x, o2
     torch.cuda.empty_cache()
+
+
+def test_garbage_inputs_never_trap(env):
+    """Outside the per-sample domain the result is unspecified but never traps
+    (vndf.h): random bit patterns (NaN, inf, subnormals, negatives) through every
+    streamed entry point; the CUDA context stays healthy afterwards."""
+    oracle, vndf, synth, dev = env
+    n = (1 << 18) + 5
+    g = torch.Generator(device="cpu").manual_seed(123)
+    bits = torch.randint(-2**31, 2**31 - 1, (7, n), generator=g, dtype=torch.int64).to(torch.int32)
+    ins = [bits[k].view(torch.float32).to(dev) for k in range(7)]
+    out = [torch.empty(n, dtype=torch.float32, device=dev) for _ in range(5)]
+    vndf.vndf_sample_cap_pdf(*ins, *out[:4])
+    vndf.vndf_sample_cap(*ins, *out[:3])
+    vndf.vndf_sample_heitz2018(*ins, *out[:4])
+    vndf.vndf_sample_cap_pdf_native(*ins, *out[:4])
+    vndf.vndf_sample_cap_reflect(*ins, *out)
+    vndf.vndf_pdf(*ins[:3], *ins[:3], ins[3], ins[4], out[0])
+    c = torch.zeros(1, dtype=torch.int64, device=dev)
+    vndf.vndf_count_fixups(*ins, c)
+    torch.cuda.synchronize()
+    # the context is still usable and correct
+    x = synth.fill(1, 0, 4096, device=dev)
+    o = vndf.empty_outputs(4096, dev)
+    vndf.vndf_sample_cap_pdf(*[x[k] for k in synth.PLANES], *o)
+    torch.cuda.synchronize()
+    h_ref, p_ref, _ = oracle.batch_sample(oracle.CAP, *[x[k].cpu().numpy() for k in synth.PLANES])
+    h = np.stack([t.cpu().numpy() for t in o[:3]]).astype(np.float64)
+    assert np.abs(h - h_ref).max() <= TOL_H
