@@ -341,3 +341,39 @@ def test_cap_density_integrates_to_one(orc, zi):
             tot += orc.cap_density([r * np.cos(p), r * np.sin(p), z], wi)
     tot *= (2.0 / nz) * (2 * np.pi / nphi)
     assert tot == pytest.approx(1.0, abs=1.5 / nz * (1 + abs(zi)) + 1e-9)
+
+
+def test_heitz_inverse_map(orc):
+    """Per-sample pin of Listing 1 + Listing 2 away from normal
+    incidence: undo the unstretch (M^T), express the std-space
+    normal in the basis (w1, w2, ws) of P:435-438 and check the disk
+    parameterisation: t1 = sqrt(u2) cos(2 pi u1) and
+    t2 = (1 - s) sqrt(1 - t1^2) + s sqrt(u2) sin(2 pi u1), s = (1 + ws.z)/2
+    (P:443-445).  Catches a swapped or mis-signed basis vector, swapped
+    uniforms and a wrong warp of the cross section."""
+    rng = np.random.default_rng(12)
+    checked = 0
+    for wi, ax, ay, u1, u2 in _random_inputs(rng, 3000):
+        h = orc.sample_vndf(HEITZ, wi, ax, ay, u1, u2)
+        sgn = -1.0 if wi[2] < 0 else 1.0
+        w = sgn * np.asarray(wi)
+        ws = np.array([ax * w[0], ay * w[1], w[2]])
+        ws /= np.linalg.norm(ws)
+        hh = sgn * h
+        hs = np.array([hh[0] / ax, hh[1] / ay, hh[2]])
+        hs /= np.linalg.norm(hs)
+        tmp = ws[0] ** 2 + ws[1] ** 2
+        if tmp < 1e-12:
+            continue
+        w1 = np.array([-ws[1], ws[0], 0.0]) / np.sqrt(tmp)
+        w2 = np.cross(ws, w1)
+        t1, t2 = hs @ w1, hs @ w2
+        r = np.sqrt(u2)
+        s = (1 + ws[2]) / 2
+        want_t1 = r * np.cos(2 * np.pi * u1)
+        want_t2 = (1 - s) * np.sqrt(max(1 - want_t1 ** 2, 0)) + s * r * np.sin(2 * np.pi * u1)
+        cond = max(ax, ay) / min(ax, ay)
+        assert t1 == pytest.approx(want_t1, abs=1e-8 * cond)
+        assert t2 == pytest.approx(want_t2, abs=1e-8 * cond)
+        checked += 1
+    assert checked > 2500

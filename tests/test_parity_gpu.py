@@ -324,3 +324,29 @@ def test_error_codes(env):
     assert L.vndf_sample_cap_philox(1, 0, -5, *Q, None) == vndf.VNDF_ERR_INVALID_ARGUMENT
     assert L.vndf_sample_cap_philox(1, 0, 64, Q[0], Q[0], Q[2], Q[3], None) == vndf.VNDF_ERR_INVALID_ARGUMENT
     torch.cuda.synchronize()
+
+
+def test_heitz_philox_conditioned_parity(env):
+    """The fused Heitz baseline on config-4 inputs (same generation as the cap
+    kernel) against the float64 Listing 2: same error-model gate as the
+    streamed baseline (reading R8)."""
+    oracle, vndf, synth, dev = env
+    n = 1 << 21
+    out = vndf.empty_outputs(n, dev)
+    vndf.vndf_sample_heitz2018_philox(3, 77, n, *out)
+    torch.cuda.synchronize()
+    idx = np.arange(77, 77 + n, dtype=np.uint64)
+    h_ref, p_ref, ti = oracle.batch_sample_philox(oracle.HEITZ, 3, idx)
+    eh, ep = _errors([o.cpu().numpy() for o in out[:3]], out[3].cpu().numpy(), h_ref, p_ref)
+    W = oracle.philox_words(3, idx, 0).astype(np.uint64)
+    ax = 0.01 * 100.0 ** ((W[:, 2] >> 8) / 2**24)
+    ay = 0.01 * 100.0 ** ((W[:, 3] >> 8) / 2**24)
+    u1, u2 = (W[:, 0] >> 8) / 2**24, (W[:, 1] >> 8) / 2**24
+    N = 1.0 / np.sqrt((h_ref[0] / ax) ** 2 + (h_ref[1] / ay) ** 2 + h_ref[2] ** 2)
+    rim = 1.0 - u2 * np.cos(2 * np.pi * u1) ** 2
+    with np.errstate(divide="ignore"):
+        est = 1e-6 * (1.0 / ti + 1.0 / np.sqrt(np.maximum(rim, 0))) / N
+    good = est <= TOL_H
+    assert good.mean() > 0.5
+    assert eh[good].max() <= TOL_H and ep[good].max() <= TOL_PDF, (float(eh[good].max()), float(ep[good].max()))
+    assert ((eh <= TOL_H) & (ep <= TOL_PDF)).mean() >= 0.98
