@@ -362,6 +362,8 @@ def variants(torch, vndf, synth, dev, stream, x2, out2):
     ins5 = [x5[k] for k in synth.PLANES]
     t_cap5 = timed(lambda: vndf.vndf_sample_cap_pdf(*ins5, *o5, stream=stream))
     t_hz5 = timed(lambda: vndf.vndf_sample_heitz2018(*ins5, *o5, stream=stream))
+    t_nat5 = timed(lambda: vndf.vndf_sample_cap_pdf_native(*ins5, *o5, stream=stream))
+    res["c5_cap_pdf_native"] = {"gsamples_s": c5.n / t_nat5 / 1e6, "ms": t_nat5}
     res["c5_cap_pdf"] = {"gsamples_s": c5.n / t_cap5 / 1e6, "ms": t_cap5}
     res["c5_heitz_pdf"] = {"gsamples_s": c5.n / t_hz5 / 1e6, "ms": t_hz5, "t_heitz_over_t_cap": t_hz5 / t_cap5}
     del x5, o5, ins5
@@ -384,6 +386,11 @@ def variants(torch, vndf, synth, dev, stream, x2, out2):
     t_r = timed(lambda: vndf.vndf_sample_cap_reflect(*ins2, *ro, stream=stream))
     rl = roofline(48 * n2, t_r, "cap_reflect_c2")
     res["c2_cap_reflect"] = {"gsamples_s": n2 / t_r / 1e6, "ms": t_r, "gb_s": rl["achieved"], "frac_hbm": rl["frac"]}
+    # NEXT-4: Eq. 1 at caller-provided h (the h just sampled), 32 B in + 4 B out
+    t_p = timed(lambda: vndf.vndf_pdf(*ro[:3], *ins2[:5], ro[3], stream=stream))
+    rl = roofline(36 * n2, t_p, "pdf_c2")
+    res["c2_pdf"] = {"gsamples_s": n2 / t_p / 1e6, "ms": t_p, "gb_s": rl["achieved"], "frac_hbm": rl["frac"]}
+    # NEXT-3: native below-horizon handling on the config-5 inputs is measured below
     del ro
     # NEXT-2: Eq. 19 white-furnace estimator (compute-bound), cap vs Heitz, 2^28 samples
     sums = torch.zeros(2, dtype=torch.float64, device=dev)
