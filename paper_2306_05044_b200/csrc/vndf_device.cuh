@@ -22,19 +22,28 @@ constexpr double kPiD = 3.14159265358979323846;
 
 // ---------------------------------------------------------------------------
 // Conditioning flag thresholds ("error budget").
-// Error model: the fp32 half vector hs = c + ws carries an absolute error of
-// a few 1e-7 (fp32 rounding of O(1) terms, MUFU sin/cos ~3.6e-7); the
-// unstretch multiplies it by at most max(ax, ay) and divides by
-// |m| = |diag(ax, ay, 1) hs|, so |dh| ~ e A with A = max(a)/|m|; the pdf
-// |m|^3 / (pi ax ay a |hs|^2) carries ~3 e A + 2 e B with B = 1/|hs|.
+// Error model: the fp32 half vector hs = c + ws carries an absolute error
+// e S, e a few 1e-7 (fp32 rounding and MUFU sin/cos ~3.6e-7 relative to the
+// summands) and S the size of the summands, S <= sqrt(2 (sin^2 theta + rs^2))
+// with rs = |ws.xy|; the unstretch multiplies it by at most max(ax, ay) and
+// divides by |m| = |diag(ax, ay, 1) hs|, so |dh| ~ e A with A = max(a) S / |m|;
+// the pdf |m|^3 / (pi ax ay a |hs|^2) carries ~3 e A + 2 e B, B = S / |hs|.
 // Calibrated on the B200 against the float64 oracle with the fix-up disabled
-// (tools/calibrate_flags.py, 2^23 samples of each BASELINE config): on
-// samples with A <= 30 and B <= 40 the worst errors were |dh| = 6.1e-6 and
-// pdf rel = 1.5e-5 (tolerances 2e-5 / 1e-4).  Samples outside
-//     |m|^2 >= kFlagM max(a)^2   and   |hs|^2 >= kFlagHs
-// (0.02% - 0.34% of samples depending on the config) are recomputed in float64.
-constexpr float kFlagM = 1.0f / 900.0f;    // A <= 30
-constexpr float kFlagHs = 1.0f / 1600.0f;  // B <= 40
+// (tools/calibrate_scaled.py, 2^23 samples of configs 1, 2, 3, 5 and config 5
+// in the native frame): with A <= 40 and B <= 60 (S = st + rs) the worst
+// errors were |dh| = 5.6e-6 and pdf rel = 4.0e-5 (tolerances 2e-5 / 1e-4);
+// the kernels test the same thresholds with the upper bound S^2 <=
+// 2 (sin^2 + rs^2) (slightly more conservative).  Fix-up rates: 0.02-0.2%
+// (flip frame), 0.3% (config 5, native frame).  Samples outside
+//     |m|^2 >= max(a)^2 S^2 / 40^2   and   |hs|^2 >= S^2 / 60^2
+// are recomputed in float64.
+// The fused kernel (kFrameUpper, config 4) keeps the earlier scale-free test
+// (A = max(a)/|m| <= 30, B = 1/|hs| <= 40; calibrated with tools/calibrate_flags.py):
+// its inputs never reach the small-S regime and it saves two instructions.
+constexpr float kFlagM = 1.0f / 900.0f;    // scale-free A <= 30 (kFrameUpper)
+constexpr float kFlagHs = 1.0f / 1600.0f;  // scale-free B <= 40 (kFrameUpper)
+constexpr float kFlagMS = 2.0f / 1600.0f;  // scaled: m2 < max(a)^2 * 2 (sin2 + rs2) / 40^2
+constexpr float kFlagHsS = 2.0f / 3600.0f; // scaled: hs2 < 2 (sin2 + rs2) / 60^2
 
 // ---------------------------------------------------------------------------
 // Explicit single-instruction SFU approximations (MUFU.RSQ / SQRT / RCP).
@@ -105,6 +114,7 @@ struct CapCore {
     float mx, my;         // m = diag(ax, ay, 1) hs
     float m2, invN;       // |m|^2, 1/|m|
     float hs2;            // |hs|^2
+    float s2;             // sin^2(theta) + |ws.xy|^2 (size of the summands of hs)
 };
 
 // Frames of the incidence: kFrameFlip = reading R4 (wi.z < 0 is flipped);
@@ -142,15 +152,18 @@ __device__ __forceinline__ CapCore cap_core(float wx, float wy, float wz, float 
     k.m2 = fmaf(k.mx, k.mx, fmaf(k.my, k.my, k.hz * k.hz));
     k.invN = rsqrt_approx(k.m2);
     k.hs2 = fmaf(k.hx, k.hx, fmaf(k.hy, k.hy, k.hz * k.hz));
+    k.s2 = sin2 + rs2;  // S^2 / 2 of the error model (scaled conditioning test)
     return k;
 }
 
+template <int FRAME>
 __device__ __forceinline__ bool cap_flag(const CapCore& k, float ax, float ay) {
-#ifdef VNDF_NO_FIXUP  // calibration builds only (tools/calibrate_flags.py)
+#ifdef VNDF_NO_FIXUP  // calibration builds only (tools/calibrate_*.py)
     return false;
 #else
     const float amax = fmaxf(ax, ay);
-    return (k.m2 < kFlagM * (amax * amax)) | (k.hs2 < kFlagHs);
+    if (FRAME == kFrameUpper) return (k.m2 < kFlagM * (amax * amax)) | (k.hs2 < kFlagHs);
+    return (k.m2 < kFlagMS * (amax * amax) * k.s2) | (k.hs2 < kFlagHsS * k.s2);
 #endif
 }
 
@@ -168,7 +181,7 @@ __device__ __forceinline__ bool cap_fp32(float wx, float wy, float wz, float ax,
         const float den = (kPiF * ax * ay) * k.a * k.hs2;
         o.pdf = num * rcp_approx(den);
     }
-    return cap_flag(k, ax, ay);
+    return cap_flag<FRAME>(k, ax, ay);
 }
 
 // ---------------------------------------------------------------------------
@@ -204,7 +217,7 @@ __device__ __forceinline__ bool cap_reflect_fp32(float wx, float wy, float wz, f
     const float Lo = sqrt_approx(fmaf(ax * o.x, ax * o.x, fmaf(ay * o.y, ay * o.y, o.z * o.z)));
     const float wgt = zo * (zi + L) * rcp_approx(fmaf(L, zo, Lo * zi));
     o.weight = zo > 0.0f ? wgt : 0.0f;
-    return cap_flag(k, ax, ay);
+    return cap_flag<FLIP ? kFrameFlip : kFrameUpper>(k, ax, ay);
 }
 
 // ---------------------------------------------------------------------------
