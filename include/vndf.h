@@ -212,7 +212,9 @@ vndf_status vndf_furnace(int method, float wi_x, float wi_y, float wi_z, float a
  * phi in [0, 2 pi)) (expected masses: Eq. 1); mode 1: the std-space reflected
  * direction c = reflect(ws, normalize(M^T h)) in bins of ((c.z + ws.z)/(1 + ws.z),
  * phi_c/(2 pi)) -- uniform by Eq. 10.  Counts are ADDED to
- * counts[nt * nphi] (device uint64), row-major in theta / z.  nt * nphi <= 8192. */
+ * counts[nt * nphi] (device uint64), row-major in theta / z.  nt * nphi <= 8192.
+ * Per-block partial counts are 32-bit: VNDF_ERR_INVALID_ARGUMENT if one block
+ * would bin 2^32 or more samples (n above ~6e11 on a B200); split the call. */
 vndf_status vndf_histogram(int method, int mode, float wi_x, float wi_y, float wi_z,
                            float alpha_x, float alpha_y, uint64_t seed, uint64_t first_index,
                            int64_t n, int nt, int nphi, uint64_t *counts, vndf_stream_t stream);

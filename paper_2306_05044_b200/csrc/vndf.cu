@@ -91,6 +91,26 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, cudaStream
     return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
+// SM count of the current device (cached per device).
+cudaError_t sm_count(int* sms) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        auto it = g_sms.find(dev);
+        if (it != g_sms.end()) {
+            *sms = it->second;
+            return cudaSuccess;
+        }
+    }
+    e = cudaDeviceGetAttribute(sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_sms[dev] = *sms;
+    return cudaSuccess;
+}
+
 // Persistent grid: min(work, SMs x resident blocks per SM).
 // persistent: default grid policy of the kernel family when no preference is
 // set (streamed kernels: one chunk per thread, measured faster on B200 for
@@ -101,18 +121,12 @@ cudaError_t grid_for(const void* kernel, int block, int64_t work_items, int* gri
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     int sms = 0, occ = 0;
+    e = sm_count(&sms);
+    if (e != cudaSuccess) return e;
     {
         std::lock_guard<std::mutex> lk(g_mu);
-        auto it = g_sms.find(dev);
-        if (it != g_sms.end()) sms = it->second;
         auto jt = g_occ.find(std::make_tuple(dev, kernel, block));
         if (jt != g_occ.end()) occ = jt->second;
-    }
-    if (sms == 0) {
-        e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (e != cudaSuccess) return e;
-        std::lock_guard<std::mutex> lk(g_mu);
-        g_sms[dev] = sms;
     }
     if (occ == 0) {
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, block, smem);
@@ -352,12 +366,13 @@ vndf_status launch_philox_v(uint64_t seed, uint64_t first, int64_t n, float* hx,
     if (e == cudaSuccess && METHOD == kCap) {
         // one thread per queue slot up to SMs x 32 blocks; blocks past the
         // device-side count exit at once
-        int sms = 0, dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        int sms = 0;
+        e = sm_count(&sms);
         const int64_t fix_blocks = std::min<int64_t>(((int64_t)fq.cap + 127) / 128, (int64_t)std::max(sms, 1) * 32);
-        philox_fixup_kernel<<<(int)fix_blocks, 128, 0, s>>>(seed, first, n, fq, gtab, hx, hy, hz, pdf);
-        e = cudaGetLastError();
+        if (e == cudaSuccess) {
+            philox_fixup_kernel<<<(int)fix_blocks, 128, 0, s>>>(seed, first, n, fq, gtab, hx, hy, hz, pdf);
+            e = cudaGetLastError();
+        }
     }
     if (qbuf) {
         const cudaError_t ef = cudaFreeAsync(qbuf, s);
@@ -753,12 +768,13 @@ vndf_status vndf_histogram(int method, int mode, float wi_x, float wi_y, float w
     const void* k = method == 0 ? (const void*)histogram_kernel<kCap>
                   : method == 1 ? (const void*)histogram_kernel<kHeitz>
                                 : (const void*)histogram_kernel<kCapNative>;
-    int dev = 0, sms = 0, occ = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int sms = 0, occ = 0;
+    cudaError_t e = sm_count(&sms);
     if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, smem);
     if (e != cudaSuccess) return cuda_fail(e);
     const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sms * std::max(occ, 1));
+    // shared-memory partial counts are 32-bit: bound the samples per block
+    if ((n + grid - 1) / grid > (int64_t)UINT32_MAX) return VNDF_ERR_INVALID_ARGUMENT;
     cudaStream_t s = (cudaStream_t)stream;
     auto* c = (unsigned long long*)counts;
     if (method == 0)

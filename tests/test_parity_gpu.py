@@ -323,7 +323,14 @@ def test_error_codes(env):
     assert L.vndf_sample_heitz2018(*P, *Q[:3], None, 64, None) == vndf.VNDF_OK
     assert L.vndf_sample_cap_philox(1, 0, -5, *Q, None) == vndf.VNDF_ERR_INVALID_ARGUMENT
     assert L.vndf_sample_cap_philox(1, 0, 64, Q[0], Q[0], Q[2], Q[3], None) == vndf.VNDF_ERR_INVALID_ARGUMENT
+    # histogram: 32-bit per-block partial counts bound the samples per call
+    counts = torch.zeros(64, dtype=torch.int64, device=dev)
+    cp = ctypes.c_void_p(counts.data_ptr())
+    assert L.vndf_histogram(0, 0, 0.0, 0.0, 1.0, 0.5, 0.5, 1, 0, 1 << 62, 8, 8, cp, None) \
+        == vndf.VNDF_ERR_INVALID_ARGUMENT
+    assert L.vndf_histogram(0, 0, 0.0, 0.0, 1.0, 0.5, 0.5, 1, 0, 1000, 8, 8, cp, None) == vndf.VNDF_OK
     torch.cuda.synchronize()
+    assert int(counts.sum().item()) == 1000
 
 
 def test_heitz_philox_conditioned_parity(env):
