@@ -280,7 +280,7 @@ constexpr float kRotC = 0.764842187f, kRotS = 0.644217687f;  // cos, sin of 0.7 
 
 template <int VARIANT>
 __global__ void __launch_bounds__(256) microbench_kernel(uint64_t seed, int64_t lanes, int iters,
-                                                         const float2* __restrict__ gtab,
+                                                         const float* __restrict__ gtab,
                                                          float* __restrict__ checksum) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= lanes) return;

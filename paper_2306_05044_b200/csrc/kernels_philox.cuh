@@ -12,10 +12,11 @@
 // lanes busy.  If the queue overflowed (count > cap), the fix-up kernel
 // rescans every sample's flag instead: always correct, slower only then.
 
+// ctr = first + k, the Philox counter of local sample k
 template <int METHOD, bool PDF>
-__device__ __forceinline__ Sample philox_one(const PhiloxKeys& ks, uint64_t first, uint64_t k,
-                                             const FixQueue& fq, const float2* __restrict__ tab) {
-    const Inputs in = c4_inputs_fp32(philox_sample_ks(ks, first + k), tab);
+__device__ __forceinline__ Sample philox_one(const PhiloxKeys& ks, uint64_t ctr, uint64_t k,
+                                             const FixQueue& fq, const float* __restrict__ tab) {
+    const Inputs in = c4_inputs_fp32<true, METHOD == kCap>(philox_sample_ks(ks, ctr), tab);
     Sample o;
     if (METHOD == kCap) {
         // config-4 inputs are on the upper hemisphere (wi.z = 1 - u > 0): no flip
@@ -31,7 +32,7 @@ __device__ __forceinline__ Sample philox_one(const PhiloxKeys& ks, uint64_t firs
 }
 
 __global__ void __launch_bounds__(128) philox_fixup_kernel(uint64_t seed, uint64_t first, int64_t n,
-                                                            FixQueue fq, const float2* __restrict__ gtab,
+                                                            FixQueue fq, const float* __restrict__ gtab,
                                                             float* __restrict__ hx,
                                                             float* __restrict__ hy, float* __restrict__ hz,
                                                             float* __restrict__ pdf) {
@@ -71,26 +72,30 @@ __global__ void __launch_bounds__(128) philox_fixup_kernel(uint64_t seed, uint64
 #define VNDF_PHILOX_V 4
 #endif
 
-template <int METHOD, bool PDF, int V>
+// ALIGNED: first is a multiple of V, so the counters of a chunk share their
+// high word and differ only in the low bits (no 64-bit add per sample).
+template <int METHOD, bool PDF, int V, bool ALIGNED>
 __global__ void __launch_bounds__(256, VNDF_PHILOX_MINB) philox_kernel(uint64_t seed, uint64_t first, int64_t n,
                                                      float* __restrict__ hxp, float* __restrict__ hyp,
                                                      float* __restrict__ hzp, float* __restrict__ pdfp,
-                                                     FixQueue fq, const float2* __restrict__ gtab,
+                                                     FixQueue fq, const float* __restrict__ gtab,
                                                      const __grid_constant__ PhiloxKeys ks) {
     // Stage the 64 KB sin/cos table of the incidence azimuth in shared memory
     // with one TMA bulk copy (cp.async.bulk, completion on an mbarrier).
-    extern __shared__ __align__(16) float2 tab[];
+    extern __shared__ __align__(16) float tab[];
     __shared__ __align__(8) uint64_t tab_bar;
-    bulk_load_shared(tab, gtab, kSinCosTableEntries * sizeof(float2), &tab_bar);
+    bulk_load_shared(tab, gtab, kSinTableBytes, &tab_bar);
     const int64_t nchunks = n / V;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     for (int64_t c = tid; c < nchunks; c += stride) {
         const int64_t i = c * V;
+        const uint64_t base = first + (uint64_t)i;
         Vec<V> hx, hy, hz, pd;
 #pragma unroll
         for (int j = 0; j < V; ++j) {
-            const Sample o = philox_one<METHOD, PDF>(ks, first, (uint64_t)(i + j), fq, tab);
+            const uint64_t ctr = ALIGNED ? (base | (uint64_t)j) : base + (uint64_t)j;
+            const Sample o = philox_one<METHOD, PDF>(ks, ctr, (uint64_t)(i + j), fq, tab);
             hx.v[j] = o.x;
             hy.v[j] = o.y;
             hz.v[j] = o.z;
@@ -104,7 +109,7 @@ __global__ void __launch_bounds__(256, VNDF_PHILOX_MINB) philox_kernel(uint64_t 
     if (V > 1) {
         const int64_t i = nchunks * V + tid;
         if (i < n) {
-            const Sample o = philox_one<METHOD, PDF>(ks, first, (uint64_t)i, fq, tab);
+            const Sample o = philox_one<METHOD, PDF>(ks, first + (uint64_t)i, (uint64_t)i, fq, tab);
             hxp[i] = o.x;
             hyp[i] = o.y;
             hzp[i] = o.z;
@@ -148,7 +153,7 @@ __global__ void __launch_bounds__(256) count_stream_kernel(StreamArgs a, int64_t
 }
 
 __global__ void __launch_bounds__(256) count_philox_kernel(uint64_t seed, uint64_t first, int64_t n,
-                                                           const float2* __restrict__ gtab,
+                                                           const float* __restrict__ gtab,
                                                            unsigned long long* count) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t start = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

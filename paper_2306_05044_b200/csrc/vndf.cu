@@ -199,35 +199,34 @@ cudaError_t allow_dynamic_smem(const void* kernel, size_t bytes) {
     return e;
 }
 
-// Octant table of (sin, cos)(2 pi j / 2^16), j = 0 .. 8192, for the config-4
+// Quadrant table sin(2 pi j / 2^16), j = 0 .. 16384, for the config-4
 // incidence azimuth: built on the host in float64 (correctly rounded to fp32),
 // uploaded once per device, kept for the life of the process (64 KB).
-std::map<int, float2*> g_sincos_tab;
+std::map<int, float*> g_sin_tab;
 
-cudaError_t sincos_table(float2** out) {
+cudaError_t sincos_table(float** out) {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     std::lock_guard<std::mutex> lk(g_mu);
-    auto it = g_sincos_tab.find(dev);
-    if (it != g_sincos_tab.end()) {
+    auto it = g_sin_tab.find(dev);
+    if (it != g_sin_tab.end()) {
         *out = it->second;
         return cudaSuccess;
     }
-    std::vector<float2> h(kSinCosTableEntries);
-    for (int j = 0; j < kSinCosTableEntries; ++j) {
-        const int jj = j < 8193 ? j : 8192;  // padding entry repeats the last one
-        const double a = 2.0 * 3.14159265358979323846 * (double)jj / 65536.0;
-        h[j] = make_float2((float)sin(a), (float)cos(a));
+    std::vector<float> h(kSinTableEntries);
+    for (int j = 0; j < kSinTableEntries; ++j) {
+        const int jj = j < 16385 ? j : 16384;  // padding entries repeat the last one
+        h[j] = (float)sin(2.0 * 3.14159265358979323846 * (double)jj / 65536.0);
     }
-    float2* d = nullptr;
-    e = cudaMalloc((void**)&d, h.size() * sizeof(float2));
-    if (e == cudaSuccess) e = cudaMemcpy(d, h.data(), h.size() * sizeof(float2), cudaMemcpyHostToDevice);
+    float* d = nullptr;
+    e = cudaMalloc((void**)&d, h.size() * sizeof(float));
+    if (e == cudaSuccess) e = cudaMemcpy(d, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
         if (d) cudaFree(d);
         return e;
     }
-    g_sincos_tab[dev] = d;
+    g_sin_tab[dev] = d;
     *out = d;
     return cudaSuccess;
 }
@@ -328,12 +327,12 @@ vndf_status validate_philox_out(int64_t n, float* hx, float* hy, float* hz, floa
     return VNDF_OK;
 }
 
-template <int METHOD, bool PDF, int V>
+template <int METHOD, bool PDF, int V, bool ALIGNED>
 vndf_status launch_philox_v(uint64_t seed, uint64_t first, int64_t n, float* hx, float* hy, float* hz,
                             float* pdf, cudaStream_t s) {
-    const void* k = (const void*)philox_kernel<METHOD, PDF, V>;
+    const void* k = (const void*)philox_kernel<METHOD, PDF, V, ALIGNED>;
     const int block = block_size();
-    const size_t smem = kSinCosTableEntries * sizeof(float2);
+    const size_t smem = kSinTableBytes;
     cudaError_t e = allow_dynamic_smem(k, smem);
     if (e != cudaSuccess) return cuda_fail(e);
     int grid = 0;
@@ -354,13 +353,13 @@ vndf_status launch_philox_v(uint64_t seed, uint64_t first, int64_t n, float* hx,
             return cuda_fail(e);
         }
     }
-    float2* gtab = nullptr;
+    float* gtab = nullptr;
     e = sincos_table(&gtab);
     if (e != cudaSuccess) {
         if (qbuf) cudaFreeAsync(qbuf, s);
         return cuda_fail(e);
     }
-    philox_kernel<METHOD, PDF, V><<<grid, block, smem, s>>>(seed, first, n, hx, hy, hz, pdf, fq, gtab,
+    philox_kernel<METHOD, PDF, V, ALIGNED><<<grid, block, smem, s>>>(seed, first, n, hx, hy, hz, pdf, fq, gtab,
                                                             philox_keys(seed));
     e = cudaGetLastError();
     if (e == cudaSuccess && METHOD == kCap) {
@@ -389,12 +388,15 @@ vndf_status launch_philox(uint64_t seed, uint64_t first, int64_t n, float* hx, f
     constexpr int PV = VNDF_PHILOX_V;
     bool v4 = aligned(hx, 4 * PV) && aligned(hy, 4 * PV) && aligned(hz, 4 * PV) && (!pdf || aligned(pdf, 4 * PV));
     if (prefs().vector_width == 1) v4 = false;
+    const bool al = first % PV == 0;  // counters of a chunk share their high word
     if (pdf) {
-        return v4 ? launch_philox_v<METHOD, true, PV>(seed, first, n, hx, hy, hz, pdf, s)
-                  : launch_philox_v<METHOD, true, 1>(seed, first, n, hx, hy, hz, pdf, s);
+        if (!v4) return launch_philox_v<METHOD, true, 1, true>(seed, first, n, hx, hy, hz, pdf, s);
+        return al ? launch_philox_v<METHOD, true, PV, true>(seed, first, n, hx, hy, hz, pdf, s)
+                  : launch_philox_v<METHOD, true, PV, false>(seed, first, n, hx, hy, hz, pdf, s);
     }
-    return v4 ? launch_philox_v<METHOD, false, PV>(seed, first, n, hx, hy, hz, pdf, s)
-              : launch_philox_v<METHOD, false, 1>(seed, first, n, hx, hy, hz, pdf, s);
+    if (!v4) return launch_philox_v<METHOD, false, 1, true>(seed, first, n, hx, hy, hz, pdf, s);
+    return al ? launch_philox_v<METHOD, false, PV, true>(seed, first, n, hx, hy, hz, pdf, s)
+              : launch_philox_v<METHOD, false, PV, false>(seed, first, n, hx, hy, hz, pdf, s);
 }
 
 // ------------------------------------------------ host-path staging cache --
@@ -572,7 +574,7 @@ vndf_status vndf_count_fixups_philox(uint64_t seed, uint64_t first_index, int64_
     int grid = 0;
     cudaError_t e = grid_for((const void*)count_philox_kernel, 256, n, &grid);
     if (e != cudaSuccess) return cuda_fail(e);
-    float2* gtab = nullptr;
+    float* gtab = nullptr;
     e = sincos_table(&gtab);
     if (e != cudaSuccess) return cuda_fail(e);
     count_philox_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(seed, first_index, n, gtab,
@@ -796,7 +798,7 @@ vndf_status vndf_microbench(int method, uint64_t seed, int64_t lanes, int iters,
     const int64_t grid = (lanes + block - 1) / block;
     if (grid > INT32_MAX) return VNDF_ERR_INVALID_ARGUMENT;
     cudaStream_t s = (cudaStream_t)stream;
-    float2* gtab = nullptr;
+    float* gtab = nullptr;
     cudaError_t e = sincos_table(&gtab);
     if (e != cudaSuccess) return cuda_fail(e);
     switch (method) {

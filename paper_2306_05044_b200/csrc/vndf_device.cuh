@@ -486,7 +486,25 @@ struct Inputs {
 };
 
 // The 24-bit integer of a word, as float: u(w) = fw(w) 2^-24 exactly.
+// Integer multiply-add / high multiply pinned to IMAD (FMA pipe): left to
+// itself the compiler turns x * 2^k + c into SHF/IADD3/LEA on the ALU pipe.
+__device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+__device__ __forceinline__ uint32_t imad_hi(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+
 __device__ __forceinline__ float fw(uint32_t w) { return __uint2float_rn(w >> 8); }
+// The same value with the shift as a high multiply (FMA pipe, see imad): the
+// fused cap kernel is short of ALU issue, the Heitz one of FMA issue.
+__device__ __forceinline__ float fw_hi(uint32_t w) { return __uint2float_rn(imad_hi(w, 1u << 24)); }
+template <bool HI>
+__device__ __forceinline__ float fw_t(uint32_t w) { return HI ? fw_hi(w) : fw(w); }
 // The 16-bit integer made of the low bytes of two words, as float.
 __device__ __forceinline__ float fw16(uint32_t lo, uint32_t hi) {
     return __uint2float_rn(__byte_perm(lo, hi, 0x7740) & 0xFFFFu);
@@ -528,27 +546,37 @@ __device__ __forceinline__ uint4 philox_sample(uint64_t seed, uint64_t i) {
                          make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
 }
 
-// sin and cos of 2 pi K / 2^16 for a 16-bit K from the octant table
-// T[j] = (sin, cos)(2 pi j / 2^16), j = 0 .. 8192 (correctly rounded fp32,
-// built on the host in float64): quadrant q = K >> 14, rq = K mod 2^14,
-// j = min(rq, 2^14 - rq); swap sin/cos when rq > 2^13 XOR q odd; signs by
-// quadrant.  Exact reduction, ~0.5 ulp: relative accuracy in each component.
-constexpr int kSinCosTableEntries = 8194;  // 8193 used, padded to a 16-byte multiple
-__device__ __forceinline__ void sincos_2pi_u16(uint32_t K, const float2* __restrict__ tab, float* s,
+// sin and cos of 2 pi K / 2^16 for a 16-bit K (bits 16-31 of K are ignored)
+// from the quadrant table S[j] = sin(2 pi j / 2^16), j = 0 .. 2^14 (correctly
+// rounded fp32, built on the host in float64), using cos(x) = sin(pi/2 - x):
+// with r = K mod 2^14 and j = r (even quadrant) or 2^14 - r (odd quadrant),
+// sin = +-S[j], cos = +-S[2^14 - j]; the signs are the quadrant's, applied to
+// the sign bit.  Exact reduction, ~0.5 ulp: relative accuracy in each
+// component.  The index and sign arithmetic is IMAD-shaped (FMA pipe) and two
+// LDS.32 replace the octant table's swap selects: the fused kernel is short of
+// ALU-pipe issue slots (profiles/r1/prof_c4_r1_summary.txt).
+constexpr int kSinTableEntries = 16388;  // 16385 used, padded to a 16-byte multiple
+constexpr unsigned kSinTableBytes = kSinTableEntries * sizeof(float);
+// 2^16 as a constant-bank value: a literal power-of-two multiplier is
+// strength-reduced to SHF/IADD3 (ALU pipe) even through mad.lo.
+__constant__ uint32_t kImad2e16 = 65536u;
+
+__device__ __forceinline__ void sincos_2pi_u16(uint32_t K, const float* __restrict__ S, float* s,
                                                float* c) {
-    const uint32_t q = K >> 14, rq = K & 0x3FFFu;
-    const uint32_t j = min(rq, 16384u - rq);
-    const float2 t = tab[j];
-    const bool swap = (rq > 8192u) != ((q & 1u) != 0u);
-    const float a = swap ? t.y : t.x, b = swap ? t.x : t.y;
-    *s = (q & 2u) ? -a : a;
-    *c = ((q + 1u) & 2u) ? -b : b;
+    const uint32_t r = K & 0x3FFFu;
+    const uint32_t odd = imad_hi(K & 0x4000u, 1u << 18);        // bit 14 of K
+    const uint32_t js = imad(odd, imad(r, 0xFFFFFFFEu, 16384u), r);  // r or 2^14 - r
+    const float a = S[js], b = S[16384u - js];
+    const uint32_t m16 = kImad2e16;
+    *s = __uint_as_float(__float_as_uint(a) ^ (imad(K, m16, 0u) & 0x80000000u));           // q = 2, 3
+    *c = __uint_as_float(__float_as_uint(b) ^ (imad(K, m16, 0x40000000u) & 0x80000000u));  // q = 1, 2
 }
 
 // tab = nullptr: sincospif; else the 16-bit table (shared or global memory).
 // (A compile-time switch: the product kernels always pass the table.)
-template <bool TABLE = true>
-__device__ __forceinline__ Inputs c4_inputs_fp32(uint4 W, const float2* __restrict__ tab) {
+// FW_HI: convert the 24-bit uniforms with fw_hi (bit-identical to fw).
+template <bool TABLE = true, bool FW_HI = false>
+__device__ __forceinline__ Inputs c4_inputs_fp32(uint4 W, const float* __restrict__ tab) {
     Inputs in;
     const float fa = fw16(W.x, W.y);
     const float ua = fa * 0x1p-16f;
@@ -561,7 +589,7 @@ __device__ __forceinline__ Inputs c4_inputs_fp32(uint4 W, const float2* __restri
     // error 2^-21.4) would not.
     float sp, cp;
     if (TABLE) {
-        sincos_2pi_u16(__byte_perm(W.z, W.w, 0x7740) & 0xFFFFu, tab, &sp, &cp);
+        sincos_2pi_u16(__byte_perm(W.z, W.w, 0x7740), tab, &sp, &cp);
     } else {
         sincospif(fw16(W.z, W.w) * 0x1p-15f, &sp, &cp);  // 2 pi ub, ub = fw16 2^-16
     }
@@ -569,10 +597,10 @@ __device__ __forceinline__ Inputs c4_inputs_fp32(uint4 W, const float2* __restri
     in.wy = r * sp;
     in.wz = z;
     // 0.01 * 100^u = 2^((u - 1) log2 100); u log2 100 = fw (2^-24 log2 100) exactly
-    in.ax = ex2_approx(fmaf(fw(W.z), kLog2_100F * 0x1p-24f, -kLog2_100F));
-    in.ay = ex2_approx(fmaf(fw(W.w), kLog2_100F * 0x1p-24f, -kLog2_100F));
-    in.v1 = fmaf(fw(W.x), 0x1p-24f, -0.5f);
-    const float f2 = fw(W.y);
+    in.ax = ex2_approx(fmaf(fw_t<FW_HI>(W.z), kLog2_100F * 0x1p-24f, -kLog2_100F));
+    in.ay = ex2_approx(fmaf(fw_t<FW_HI>(W.w), kLog2_100F * 0x1p-24f, -kLog2_100F));
+    in.v1 = fmaf(fw_t<FW_HI>(W.x), 0x1p-24f, -0.5f);
+    const float f2 = fw_t<FW_HI>(W.y);
     in.u2 = f2 * 0x1p-24f;
     in.q = fmaf(f2, -0x1p-24f, 1.0f);
     return in;
