@@ -149,13 +149,42 @@ def test_config4_philox_sampled(env):
 def test_philox_full_range_small(env):
     """Every sample of a 2^20 Philox range, across the 32-bit carry of the counter."""
     oracle, vndf, synth, dev = env
-    for first, n in ((0, 1 << 20), ((1 << 32) - 4096, 8192 + 3)):
+    # first % 4 != 0 selects the kernel without the shared-high-word counters
+    for first, n in ((0, 1 << 20), ((1 << 32) - 4096, 8192 + 3), ((1 << 32) - 4097, 8192 + 5), (3, 65539)):
         out = vndf.empty_outputs(n, dev)
         vndf.vndf_sample_cap_philox(3, first, n, *out)
         torch.cuda.synchronize()
         h_ref, p_ref, _ = oracle.batch_sample_philox(oracle.CAP, 3, np.arange(first, first + n, dtype=np.uint64))
         eh, ep = _errors([o.cpu().numpy() for o in out[:3]], out[3].cpu().numpy(), h_ref, p_ref)
         assert eh.max() <= TOL_H and ep.max() <= TOL_PDF, (first, float(eh.max()), float(ep.max()))
+
+
+def test_philox_first_index_offsets_bit_identical(env):
+    """Sample k of a call with first_index f is sample f + k of a call with
+    first_index 0, for every residue of f mod 4 (aligned and unaligned chunk
+    counters) and for unaligned output pointers."""
+    oracle, vndf, synth, dev = env
+    n = (1 << 16) + 3
+    ref = vndf.empty_outputs(n + 8, dev)
+    vndf.vndf_sample_cap_philox(7, 0, n + 8, *ref)
+    for f in (1, 2, 3, 4, 5, 7):
+        out = vndf.empty_outputs(n, dev)
+        vndf.vndf_sample_cap_philox(7, f, n, *out)
+        torch.cuda.synchronize()
+        for u, v in zip(out, ref):
+            assert torch.equal(u, v[f:f + n]), f
+    out = [torch.empty(n + 1, dtype=torch.float32, device=dev)[1:] for _ in range(4)]  # 4 B aligned
+    vndf.vndf_sample_cap_philox(7, 2, n, *out)
+    torch.cuda.synchronize()
+    for u, v in zip(out, ref):
+        assert torch.equal(u, v[2:2 + n])
+    href = vndf.empty_outputs(n + 8, dev)
+    vndf.vndf_sample_heitz2018_philox(7, 0, n + 8, *href)
+    hout = vndf.empty_outputs(n, dev)
+    vndf.vndf_sample_heitz2018_philox(7, 3, n, *hout)
+    torch.cuda.synchronize()
+    for u, v in zip(hout, href):
+        assert torch.equal(u, v[3:3 + n])
 
 
 def test_philox_words_bit_exact(env):
