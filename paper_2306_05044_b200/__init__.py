@@ -102,31 +102,50 @@ def _check(fn: str, status: int) -> None:
 
 
 # ------------------------------------------------------------- marshalling --
+# Kept lean: a call's host cost is paid per launch (tools/binding_overhead.py).
+_torch = None
+
+
+def _t():
+    global _torch
+    if _torch is None:
+        import torch
+        _torch = torch
+    return _torch
+
+
 def _dev_ptr(t, n: int, name: str, dtype=None, device=None):
-    import torch
+    """(device pointer as int, CUDA device index) of a checked tensor."""
     if t is None:
         return None, device
+    torch = _t()
     if not isinstance(t, torch.Tensor):
         raise TypeError(f"{name}: expected a torch.Tensor")
     want = dtype or torch.float32
     if t.dtype != want:
         raise TypeError(f"{name}: expected {want}, got {t.dtype}")
-    if not t.is_cuda:
+    d = t.get_device()
+    if d < 0:
         raise ValueError(f"{name}: expected a CUDA tensor")
     if not t.is_contiguous() or t.numel() < n:
         raise ValueError(f"{name}: expected a contiguous tensor with >= {n} elements")
-    if device is not None and t.device != device:
-        raise ValueError(f"{name}: all tensors must be on {device}")
-    return ctypes.c_void_p(t.data_ptr()), t.device
+    if device is not None and d != device:
+        raise ValueError(f"{name}: all tensors must be on cuda:{device}")
+    return t.data_ptr(), d
 
 
 def _stream(stream, device):
-    import torch
+    """Raw cudaStream_t: the given stream, else the current stream of `device`
+    (a CUDA device index, or None for the current device)."""
+    torch = _t()
     if stream is None:
-        stream = torch.cuda.current_stream(device)
+        raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)  # skips the Stream object
+        if raw is not None:
+            return raw(torch.cuda.current_device() if device is None else device)
+        return torch.cuda.current_stream(device).cuda_stream
     if isinstance(stream, torch.cuda.Stream):
-        return ctypes.c_void_p(stream.cuda_stream)
-    return ctypes.c_void_p(int(stream))
+        return stream.cuda_stream
+    return int(stream)
 
 
 def _n(n, t) -> int:
