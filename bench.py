@@ -207,9 +207,31 @@ def cpu_baseline(host_planes, n_sample: int, budget_s: float = 12.0):
         if time.perf_counter() - t0 >= budget_s:
             break
     dt = time.perf_counter() - t0
+    # one thread on a smaller slice (report 1 and T threads)
+    n1 = min(n_sample, 1 << 20)
+    one = [np.ascontiguousarray(p[:n1]) for p in planes]
+    done1, t1 = 0, time.perf_counter()
+    while True:
+        oracle.batch_sample(oracle.CAP, *one, pdf=True, threads=1)
+        done1 += n1
+        if time.perf_counter() - t1 >= budget_s / 6:
+            break
+    dt1 = time.perf_counter() - t1
     return {"value": done / dt / 1e9, "unit": UNIT, "cores": threads, "kind": "oracle",
             "sample": f"first {n_sample} samples of config 2 (float64 Listing 1+3 + Eq. 1 pdf), "
-                      f"{done // n_sample} passes in {dt:.1f} s, {threads} threads"}
+                      f"{done // n_sample} passes in {dt:.1f} s, {threads} threads",
+            "value_1_thread": done1 / dt1 / 1e9, "cpu_model": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 def roofline(bytes_per_launch: float, launch_ms: float, kernel_key: str):
@@ -219,6 +241,16 @@ def roofline(bytes_per_launch: float, launch_ms: float, kernel_key: str):
             "frac": round(achieved / peak, 4), "traffic": profiled_traffic(kernel_key),
             "peak_source": src, "kernel": kernel_key,
             "algorithmic_bytes_per_launch": int(bytes_per_launch)}
+
+
+def _traffic_entry(key: str):
+    """Per-pipe utilisation (fractions of peak) from the committed ncu capture
+    (profiles/traffic.json): the BASELINE metric's FP32 (fma) / SFU (xu) shares."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(key)
+    except Exception:
+        return None
 
 
 def issue_roofline(gsamples_s: float, key: str, sm_mhz: float = None):
@@ -375,9 +407,12 @@ def variants(torch, vndf, synth, dev, stream, x2, out2):
     t_hz4 = timed(lambda: vndf.vndf_sample_heitz2018_philox(c4.seed, 0, c4.n, *o4, stream=stream))
     res["c4_cap_philox"] = {"gsamples_s": c4.n / t_cap4 / 1e6, "ms": t_cap4,
                             "write_gb_s": 16 * c4.n / t_cap4 / 1e6,
-                            "roofline": issue_roofline(c4.n / t_cap4 / 1e6, "cap_philox_c4_warp_inst_per_sample")}
+                            "roofline": issue_roofline(c4.n / t_cap4 / 1e6, "cap_philox_c4_warp_inst_per_sample"),
+                            "pipes_ncu": _traffic_entry("cap_philox_c4_pipes")}
     res["c4_heitz_philox"] = {"gsamples_s": c4.n / t_hz4 / 1e6, "ms": t_hz4,
-                              "t_heitz_over_t_cap": t_hz4 / t_cap4}
+                              "t_heitz_over_t_cap": t_hz4 / t_cap4,
+                              "roofline": issue_roofline(c4.n / t_hz4 / 1e6, "heitz_philox_c4_warp_inst_per_sample"),
+                              "pipes_ncu": _traffic_entry("heitz_philox_c4_pipes")}
     del o4
     torch.cuda.empty_cache()
 
