@@ -63,19 +63,29 @@ __global__ void __launch_bounds__(128) philox_fixup_kernel(uint64_t seed, uint64
     }
 }
 
-// 3 resident 256-thread blocks per SM (<= 85 registers; 3 x 64 KB of staged
-// table fit the 228 KB of shared memory): +1% over the unconstrained build.
-#ifndef VNDF_PHILOX_MINB
-#define VNDF_PHILOX_MINB 3
+// One block per SM, holding the SM's single copy of the 64 KB table: the cap
+// kernel with 768 threads (24 warps, <= 85 registers), the Heitz kernel with
+// 1024 (32 warps, <= 64 registers).  Swept on B200 (tools/variants.py) over
+// 256 x 3, 320-512 x 2 and 640-1024 x 1 blocks per SM: cap 184 (256 x 3) ->
+// 190 Gsamples/s, Heitz 175 -> 178.
+#ifndef VNDF_PHILOX_BLOCK_CAP
+#define VNDF_PHILOX_BLOCK_CAP 768
+#endif
+#ifndef VNDF_PHILOX_BLOCK_HEITZ
+#define VNDF_PHILOX_BLOCK_HEITZ 1024
 #endif
 #ifndef VNDF_PHILOX_V
 #define VNDF_PHILOX_V 4
 #endif
+template <int METHOD>
+struct PhiloxLaunch {
+    static constexpr int kBlock = METHOD == kCap ? VNDF_PHILOX_BLOCK_CAP : VNDF_PHILOX_BLOCK_HEITZ;
+};
 
 // ALIGNED: first is a multiple of V, so the counters of a chunk share their
 // high word and differ only in the low bits (no 64-bit add per sample).
 template <int METHOD, bool PDF, int V, bool ALIGNED>
-__global__ void __launch_bounds__(256, VNDF_PHILOX_MINB) philox_kernel(uint64_t seed, uint64_t first, int64_t n,
+__global__ void __launch_bounds__(PhiloxLaunch<METHOD>::kBlock, 1) philox_kernel(uint64_t seed, uint64_t first, int64_t n,
                                                      float* __restrict__ hxp, float* __restrict__ hyp,
                                                      float* __restrict__ hzp, float* __restrict__ pdfp,
                                                      FixQueue fq, const float* __restrict__ gtab,

@@ -331,7 +331,7 @@ template <int METHOD, bool PDF, int V, bool ALIGNED>
 vndf_status launch_philox_v(uint64_t seed, uint64_t first, int64_t n, float* hx, float* hy, float* hz,
                             float* pdf, cudaStream_t s) {
     const void* k = (const void*)philox_kernel<METHOD, PDF, V, ALIGNED>;
-    const int block = block_size();
+    const int block = block_size(PhiloxLaunch<METHOD>::kBlock);
     const size_t smem = kSinTableBytes;
     cudaError_t e = allow_dynamic_smem(k, smem);
     if (e != cudaSuccess) return cuda_fail(e);
