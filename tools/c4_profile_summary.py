@@ -1,0 +1,53 @@
+"""Write profiles/<round>/prof_c4_<round>_summary.txt and the fused kernels'
+instruction counts and pipe utilisation in profiles/traffic.json from an
+`ncu --set full` capture of `tools/prof_kernels.py c4` (2^26 samples per launch).
+
+python tools/c4_profile_summary.py r1 gpurun_out/prof_c4_r1.ncu-rep
+"""
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+import ncu_summary  # noqa: E402
+
+rnd, rep = sys.argv[1], sys.argv[2]
+N = 1 << 26
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(raw)))
+hdr = rows[0]
+data = rows[2:]
+EXTRA = ["sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed",
+         "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_elapsed",
+         "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum",
+         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
+         "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"]
+PIPES = {"issue": "smsp__issue_active.avg.pct_of_peak_sustained_active",
+         "fma_inst": "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+         "fmaheavy_cycles": "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed",
+         "alu": "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+         "xu_sfu": "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"}
+res = ncu_summary.load(rep)
+tpath = os.path.join(ROOT, "profiles", "traffic.json")
+traffic = json.load(open(tpath))
+out = os.path.join(ROOT, "profiles", rnd, f"prof_c4_{rnd}_summary.txt")
+with open(out, "w") as f:
+    f.write(f"ncu --set full summary of {os.path.basename(rep)} (tools/prof_kernels.py c4: 2^26 samples per launch)\n")
+    for j, d in enumerate(res):
+        f.write(d["kernel"] + "\n")
+        for k, v in d.items():
+            if k != "kernel":
+                f.write(f"    {k:85s} {v}\n")
+        for k in EXTRA:
+            f.write(f"    {k:85s} {data[j][hdr.index(k)]}\n")
+        ipw = float(str(d["smsp__inst_executed.sum"]).split()[0]) / N
+        f.write(f"    {'warp-instructions per sample':85s} {ipw:.4f}\n")
+        name = "cap" if "philox_kernel<0" in d["kernel"] else "heitz"
+        traffic[f"{name}_philox_c4_warp_inst_per_sample"] = round(ipw, 4)
+        traffic[f"{name}_philox_c4_pipes"] = {k: round(float(data[j][hdr.index(v)]) / 100, 4) for k, v in PIPES.items()}
+json.dump(traffic, open(tpath, "w"), indent=1)
+print(open(out).read())
