@@ -19,9 +19,12 @@ constexpr int kBlockFixCap = 512;
 #ifndef VNDF_STREAM_MINB
 #define VNDF_STREAM_MINB 1
 #endif
+#ifndef VNDF_STREAM_BOUND
+#define VNDF_STREAM_BOUND 256
+#endif
 
 template <int METHOD, bool PDF, int V>
-__global__ void __launch_bounds__(256, VNDF_STREAM_MINB) stream_kernel(StreamArgs a, int64_t n) {
+__global__ void __launch_bounds__(VNDF_STREAM_BOUND, VNDF_STREAM_MINB) stream_kernel(StreamArgs a, int64_t n) {
     __shared__ int64_t fix_idx[METHOD != kHeitz ? kBlockFixCap : 1];
     __shared__ int fix_count;
     if (METHOD != kHeitz && threadIdx.x == 0) fix_count = 0;
