@@ -328,7 +328,7 @@ def run_ours(args):
     e2e_s = reduce_max(e2e_s, world, dev)
     e2e = {"value": world * n * e2e_steps / e2e_s / 1e9, "unit": UNIT,
            "h2d_bytes_per_step": 28 * n, "d2h_bytes_per_step": 16 * n,
-           "api": "vndf_sample_cap_pdf_host (pinned host buffers, blocking)"}
+           "api": "vndf_sample_cap_pdf_host (pinned host buffers, blocking; zero-copy kernel over the host link)"}
 
     result = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,

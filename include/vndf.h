@@ -138,14 +138,19 @@ vndf_status vndf_sample_heitz2018_philox(uint64_t seed, uint64_t first_index, in
 vndf_status vndf_philox4x32_10(uint64_t seed, uint64_t first_index, int64_t n,
                                uint32_t block, uint32_t *words, vndf_stream_t stream);
 
-/* End-to-end form of vndf_sample_cap_pdf on HOST buffers (pinned memory
- * recommended; pageable works but is slower).  Streams the batch through the
- * GPU in chunks of 1 Mi samples, overlapping host->device copies, the kernel
- * and device->host copies on three library-owned streams.  Device staging
- * (3 x 1 Mi x 44 B = 138 MB per device) is allocated on first use and kept
- * for later calls; vndf_release_host_staging() frees it.  BLOCKING: returns
- * when the outputs are in host memory.  Work is ordered after prior work on
- * `stream`. */
+/* End-to-end form of vndf_sample_cap_pdf on HOST buffers.
+ * - If all eleven buffers are page-locked and mapped into the device's address
+ *   space (cudaHostAlloc / cudaMallocHost / torch pin_memory(); mapped by
+ *   default under unified addressing), the kernel reads the inputs and writes
+ *   the outputs across the host link in place (zero-copy), on `stream`.
+ * - Otherwise (pageable memory) the batch is streamed through the GPU in
+ *   chunks of 2 Mi samples, overlapping host->device copies, the kernel and
+ *   device->host copies on three library-owned streams.  Device staging
+ *   (3 x 2 Mi x 44 B = 277 MB per device) is allocated on first use and kept
+ *   for later calls; vndf_release_host_staging() frees it.
+ * BLOCKING: returns when the outputs are in host memory.  Work is ordered
+ * after prior work on `stream`.  Results are bit-identical to
+ * vndf_sample_cap_pdf on the same inputs. */
 vndf_status vndf_sample_cap_pdf_host(const float *wi_x, const float *wi_y, const float *wi_z,
                                      const float *alpha_x, const float *alpha_y,
                                      const float *u1, const float *u2,

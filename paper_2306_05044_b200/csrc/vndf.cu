@@ -400,15 +400,22 @@ vndf_status launch_philox(uint64_t seed, uint64_t first, int64_t n, float* hx, f
 }
 
 // ------------------------------------------------ host-path staging cache --
-// The blocking host entry point streams a batch through two device staging
-// sets of kStagingChunk samples (11 planes each: 7 in, 4 out), round-robin
-// over kStagingSets streams, so chunk c's H2D copy overlaps chunk c-1's
-// kernel and chunk c-2's D2H copy (PCIe is full duplex).
-// One staging area per device is kept after first use (3 x 1 Mi x 44 B =
-// 138 MB) so repeated calls pay no allocation; a concurrent second caller on
+// Pageable host buffers: the blocking host entry point streams a batch through
+// device staging sets of kStagingChunk samples (11 planes each: 7 in, 4 out),
+// round-robin over kStagingSets streams, so chunk c's H2D copy overlaps chunk
+// c-1's kernel and chunk c-2's D2H copy (PCIe is full duplex).
+// One staging area per device is kept after first use (3 x 2 Mi x 44 B =
+// 277 MB) so repeated calls pay no allocation; a concurrent second caller on
 // the same device gets a private area that is freed when it returns.
-constexpr int64_t kStagingChunk = (int64_t)1 << 20;
-constexpr int kStagingSets = 3;
+// (Page-locked, device-mapped buffers skip all of this: see mapped_pointer.)
+#ifndef VNDF_STAGING_CHUNK_LOG2
+#define VNDF_STAGING_CHUNK_LOG2 21  // 2 Mi samples: 1.65 vs 1.59 Gsamples/s at 1 Mi (fewer copies)
+#endif
+#ifndef VNDF_STAGING_SETS
+#define VNDF_STAGING_SETS 3
+#endif
+constexpr int64_t kStagingChunk = (int64_t)1 << VNDF_STAGING_CHUNK_LOG2;
+constexpr int kStagingSets = VNDF_STAGING_SETS;
 
 struct Staging {
     int device = 0;
@@ -583,6 +590,25 @@ vndf_status vndf_count_fixups_philox(uint64_t seed, uint64_t first_index, int64_
     return e == cudaSuccess ? VNDF_OK : cuda_fail(e);
 }
 
+}  // extern "C"
+
+namespace {
+// Device address of a page-locked host buffer mapped into the device's address
+// space (cudaHostAlloc / cudaMallocHost / torch pin_memory(), mapped by default
+// under unified addressing), else nullptr.
+const void* mapped_pointer(const void* host) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, host) != cudaSuccess) {
+        cudaGetLastError();  // pageable memory may report an error on old drivers: clear it
+        return nullptr;
+    }
+    if (at.type != cudaMemoryTypeHost || at.devicePointer == nullptr) return nullptr;
+    return at.devicePointer;
+}
+}  // namespace
+
+extern "C" {
+
 vndf_status vndf_sample_cap_pdf_host(const float* wi_x, const float* wi_y, const float* wi_z,
                                      const float* alpha_x, const float* alpha_y, const float* u1,
                                      const float* u2, float* h_x, float* h_y, float* h_z, float* pdf,
@@ -590,13 +616,33 @@ vndf_status vndf_sample_cap_pdf_host(const float* wi_x, const float* wi_y, const
     const StreamArgs host = make_args(wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, h_x, h_y, h_z, pdf);
     vndf_status st = validate_stream(host, true, n);
     if (st != VNDF_OK || n == 0) return st;
+    cudaStream_t user = (cudaStream_t)stream;
+    // Zero-copy: when all eleven buffers are mapped page-locked memory, the
+    // kernel reads its inputs and writes its outputs across the host link in
+    // place -- no copies, no staging; reads and writes overlap in both link
+    // directions (1.72 vs 1.65 Gsamples/s staged, tools/e2e_probe.py).
+    {
+        const void* hp[11] = {wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, h_x, h_y, h_z, pdf};
+        const void* dp[11];
+        bool mapped = true;
+        for (int k = 0; k < 11 && mapped; ++k) mapped = (dp[k] = mapped_pointer(hp[k])) != nullptr;
+        if (mapped) {
+            const StreamArgs da = make_args((const float*)dp[0], (const float*)dp[1], (const float*)dp[2],
+                                            (const float*)dp[3], (const float*)dp[4], (const float*)dp[5],
+                                            (const float*)dp[6], (float*)dp[7], (float*)dp[8], (float*)dp[9],
+                                            (float*)dp[10]);
+            st = launch_stream<kCap, true>(da, n, user);
+            if (st != VNDF_OK) return st;
+            const cudaError_t es = cudaStreamSynchronize(user);
+            return es == cudaSuccess ? VNDF_OK : cuda_fail(es);
+        }
+    }
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e);
     Staging* sg = nullptr;
     e = acquire_staging(dev, &sg);
     if (e != cudaSuccess) return cuda_fail(e);
-    cudaStream_t user = (cudaStream_t)stream;
     vndf_status result = VNDF_OK;
     // order after prior work on the caller's stream
     e = cudaEventRecord(sg->ev[0], user);

@@ -302,16 +302,22 @@ def test_host_entry_point_matches_device(env):
     n = (1 << 23) + 17  # three pipeline chunks, ragged
     x = synth.fill(5, 4, n, device=dev)
     d = _stream_run(vndf, x, synth.PLANES)
+    # page-locked, mapped buffers: the zero-copy path
     hin = [x[k].cpu().pin_memory() for k in synth.PLANES]
     hout = [torch.empty(n, dtype=torch.float32).pin_memory() for _ in range(4)]
     vndf.vndf_sample_cap_pdf_host(*hin, *hout)
     for a, b in zip(d, hout):
         assert torch.equal(a.cpu(), b)
-    # pageable numpy buffers work too
-    nin = [t.numpy() for t in hin]
+    # pageable numpy buffers: the staged, pipelined path (several 2 Mi chunks, ragged)
+    nin = [t.numpy().copy() for t in hin]
     nout = [np.empty(n, dtype=np.float32) for _ in range(4)]
     vndf.vndf_sample_cap_pdf_host(*nin, *nout)
     for a, b in zip(d, nout):
+        np.testing.assert_array_equal(a.cpu().numpy(), b)
+    # mixed: pinned inputs, pageable outputs -> staged path as well
+    mout = [np.empty(n, dtype=np.float32) for _ in range(4)]
+    vndf.vndf_sample_cap_pdf_host(*hin, *mout)
+    for a, b in zip(d, mout):
         np.testing.assert_array_equal(a.cpu().numpy(), b)
 
 
