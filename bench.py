@@ -441,6 +441,19 @@ def variants(torch, vndf, synth, dev, stream, x2, out2):
     fur["t_heitz_over_t_cap"] = fur["heitz"]["ms"] / fur["cap"]["ms"]
     res["furnace_eq19"] = fur
 
+    # NEXT-3: device histograms (2^28 samples of one (wi, alpha) into 64 x 64
+    # shared-memory bins; the chi-square tests' workhorse)
+    cnt = torch.zeros(64 * 64, dtype=torch.int64, device=dev)
+    hist = {}
+    for method, name in ((0, "cap"), (1, "heitz"), (2, "cap_native")):
+        wi_h = (0.5, 0.2, 0.8426149773176359) if method != 2 else (0.5, 0.2, -0.8426149773176359)
+        t_h = timed(lambda: vndf.vndf_histogram(method, 0, wi_h, (0.3, 0.1), 17, 1 << 28, 64, 64, cnt,
+                                                stream=stream))
+        hist[name] = {"gsamples_s": (1 << 28) / t_h / 1e6, "ms": t_h}
+    hist["note"] = ("audit kernel: time dominated by binning (acos, atan2, shared atomics); the cap "
+                    "path's float64 fix-ups run inline here, so this is no sampler comparison")
+    res["histogram_next3"] = hist
+
     # NEXT-1: sampler-only microbenchmark in the paper's methodology:
     # 64 Listing-1 calls per lane, median of 100 dispatches
     lanes, iters = 148 * 2048 * 16, 64
