@@ -240,7 +240,10 @@ def roofline(bytes_per_launch: float, launch_ms: float, kernel_key: str):
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": profiled_traffic(kernel_key),
             "peak_source": src, "kernel": kernel_key,
-            "algorithmic_bytes_per_launch": int(bytes_per_launch)}
+            "algorithmic_bytes_per_launch": int(bytes_per_launch),
+            # context only: the HGX B200 HBM3e figure (B200_PROFILING.md); the
+            # measured copy above is the denominator
+            "spec_gbs": 7700.0, "frac_of_spec": round(achieved / 7700.0, 4)}
 
 
 def _traffic_entry(key: str):
