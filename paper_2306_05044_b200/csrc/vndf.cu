@@ -385,7 +385,7 @@ vndf_status launch_philox(uint64_t seed, uint64_t first, int64_t n, float* hx, f
                           float* pdf, cudaStream_t s) {
     vndf_status st = validate_philox_out(n, hx, hy, hz, pdf);
     if (st != VNDF_OK || n == 0) return st;
-    constexpr int PV = VNDF_PHILOX_V;
+    constexpr int PV = PhiloxLaunch<METHOD>::kV;
     bool v4 = aligned(hx, 4 * PV) && aligned(hy, 4 * PV) && aligned(hz, 4 * PV) && (!pdf || aligned(pdf, 4 * PV));
     if (prefs().vector_width == 1) v4 = false;
     const bool al = first % PV == 0;  // counters of a chunk share their high word
