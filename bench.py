@@ -444,6 +444,19 @@ def variants(torch, vndf, synth, dev, stream, x2, out2):
     fur["t_heitz_over_t_cap"] = fur["heitz"]["ms"] / fur["cap"]["ms"]
     res["furnace_eq19"] = fur
 
+    # NEXT-2 fused: config-4 inputs in-kernel, reflection + Eq. 20 pdf + weight
+    nr = 1 << 28
+    orf = [torch.empty(nr, dtype=torch.float32, device=dev) for _ in range(5)]
+    t_rc = timed(lambda: vndf.vndf_sample_cap_reflect_philox(3, 0, nr, *orf, stream=stream))
+    t_rh = timed(lambda: vndf.vndf_sample_heitz2018_reflect_philox(3, 0, nr, *orf, stream=stream))
+    res["reflect_philox"] = {
+        "cap": {"gsamples_s": nr / t_rc / 1e6, "ms": t_rc, "write_gb_s": 20 * nr / t_rc / 1e6,
+                "roofline": issue_roofline(nr / t_rc / 1e6, "cap_reflect_philox_warp_inst_per_sample")},
+        "heitz": {"gsamples_s": nr / t_rh / 1e6, "ms": t_rh,
+                  "roofline": issue_roofline(nr / t_rh / 1e6, "heitz_reflect_philox_warp_inst_per_sample")},
+        "t_heitz_over_t_cap": t_rh / t_rc}
+    del orf
+
     # NEXT-3: device histograms (2^28 samples of one (wi, alpha) into 64 x 64
     # shared-memory bins; the chi-square tests' workhorse)
     cnt = torch.zeros(64 * 64, dtype=torch.int64, device=dev)

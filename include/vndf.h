@@ -188,6 +188,23 @@ vndf_status vndf_sample_cap_reflect(const float *wi_x, const float *wi_y, const 
                                     float *wo_x, float *wo_y, float *wo_z, float *pdf, float *weight,
                                     int64_t n, vndf_stream_t stream);
 
+/* Fused form of vndf_sample_cap_reflect on the config-4 inputs of
+ * vndf_sample_cap_philox (wi, alpha_x, alpha_y, u1, u2 of sample j drawn from
+ * the Philox block of counter first_index + j, key seed): no inputs read,
+ * 20 B written per sample (wo.xyz, Eq. 20 pdf, G2/G1 weight).  All five
+ * device pointers required, 4-byte aligned, non-overlapping.  Same accuracy
+ * contract as vndf_sample_cap_reflect; ill-conditioned samples are recomputed
+ * in float64 from the same Philox words (transient stream-ordered queue). */
+vndf_status vndf_sample_cap_reflect_philox(uint64_t seed, uint64_t first_index, int64_t n,
+                                           float *wo_x, float *wo_y, float *wo_z, float *pdf,
+                                           float *weight, vndf_stream_t stream);
+
+/* Heitz-2018 (Listing 2) baseline of vndf_sample_cap_reflect_philox on the
+ * same inputs (literal fp32, no fix-up; for the speed ratio). */
+vndf_status vndf_sample_heitz2018_reflect_philox(uint64_t seed, uint64_t first_index, int64_t n,
+                                                 float *wo_x, float *wo_y, float *wo_z, float *pdf,
+                                                 float *weight, vndf_stream_t stream);
+
 /* The VNDF pdf alone, Eq. 1, at caller-provided directions (e.g.
  * for multiple-importance-sampling weights): pdf[k] = D_vis(h_k, wi_k)
  * with reading R4 for wi.z < 0; 0 for back-facing h or h below the (flipped)

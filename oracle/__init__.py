@@ -99,6 +99,7 @@ def lib() -> ctypes.CDLL:
         L.orc_pdf_reflect.restype = d
         L.orc_sample_reflect.argtypes = [i32, P, d, d, d, d, P]
         L.orc_batch_sample_reflect.argtypes = [i32, i64] + [P] * 7 + [P]
+        L.orc_batch_sample_reflect_philox.argtypes = [i32, u64, i64, P, P, i32]
         L.orc_furnace.argtypes = [i32, P, d, d, u64, u64, i64, P]
         L.orc_batch_pdf_reflect.argtypes = [i64, P, d, d, P, P, P, P]
         L.orc_sample_vndf_native.argtypes = [i32, P, d, d, d, d, P]
@@ -305,6 +306,14 @@ def batch_sample_reflect(method, wx, wy, wz, ax, ay, u1, u2) -> np.ndarray:
     n = planes[0].size
     out = np.empty((n, 5), dtype=np.float64)
     lib().orc_batch_sample_reflect(method, n, *[_p(a) for a in planes], _p(out))
+    return out.T.copy()
+
+
+def batch_sample_reflect_philox(method, seed: int, indices, *, threads: int | None = None) -> np.ndarray:
+    """(5, n) reflection outputs on config-4 inputs (orc_c4_inputs) at global indices."""
+    idx = np.ascontiguousarray(np.asarray(indices, dtype=np.uint64).reshape(-1))
+    out = np.empty((idx.size, 5), dtype=np.float64)
+    lib().orc_batch_sample_reflect_philox(method, seed, idx.size, _p(idx), _p(out), threads or default_threads())
     return out.T.copy()
 
 

@@ -586,6 +586,7 @@ typedef struct {
     uint64_t seed;
     const uint64_t *idx;
     double *hx, *hy, *hz, *pdf, *aux;
+    double *out5; /* non-NULL: reflection outputs (orc_sample_reflect) instead of h */
 } job_t;
 
 static void run_one(const job_t *j, int64_t k)
@@ -599,6 +600,10 @@ static void run_one(const job_t *j, int64_t k)
     } else {
         wi[0] = j->wx[k]; wi[1] = j->wy[k]; wi[2] = j->wz[k];
         a_x = j->ax[k]; a_y = j->ay[k]; u1 = j->u1[k]; u2 = j->u2[k];
+    }
+    if (j->out5) {
+        orc_sample_reflect(j->method, wi, a_x, a_y, u1, u2, j->out5 + 5 * k);
+        return;
     }
     orc_sample_vndf(j->method, wi, a_x, a_y, u1, u2, h, &ti);
     j->hx[k] = h[0]; j->hy[k] = h[1]; j->hz[k] = h[2];
@@ -659,6 +664,17 @@ void orc_batch_sample_philox(int method, uint64_t seed, int64_t n,
     memset(&b, 0, sizeof b);
     b.method = method; b.seed = seed; b.idx = indices;
     b.hx = hx; b.hy = hy; b.hz = hz; b.pdf = pdf; b.aux = aux;
+    run_parallel(b, n, threads);
+}
+
+/* Reflection sampling (orc_sample_reflect) on config-4 (Philox) inputs at an
+ * explicit list of global indices: out5[5k .. 5k+4] = wo.xyz, pdf, weight. */
+void orc_batch_sample_reflect_philox(int method, uint64_t seed, int64_t n, const uint64_t *indices,
+                                     double *out5, int threads)
+{
+    job_t b;
+    memset(&b, 0, sizeof b);
+    b.method = method; b.seed = seed; b.idx = indices; b.out5 = out5;
     run_parallel(b, n, threads);
 }
 

@@ -30,6 +30,7 @@ SYMBOLS = (
     "vndf_set_launch_config", "vndf_status_string", "vndf_last_cuda_error", "vndf_version",
     "vndf_microbench", "vndf_sample_cap_reflect", "vndf_furnace", "vndf_pdf",
     "vndf_sample_cap_pdf_native", "vndf_histogram",
+    "vndf_sample_cap_reflect_philox", "vndf_sample_heitz2018_reflect_philox",
 )
 
 
@@ -68,6 +69,8 @@ def lib() -> ctypes.CDLL:
         L.vndf_release_host_staging.argtypes = []
         L.vndf_microbench.argtypes = [i32, u64, i64, i32, P, P]
         L.vndf_sample_cap_reflect.argtypes = [P] * 12 + [i64, P]
+        for name in ("vndf_sample_cap_reflect_philox", "vndf_sample_heitz2018_reflect_philox"):
+            getattr(L, name).argtypes = [u64, u64, i64, P, P, P, P, P, P]
         L.vndf_pdf.argtypes = [P] * 9 + [i64, P]
         f32_ = ctypes.c_float
         L.vndf_histogram.argtypes = [i32, i32, f32_, f32_, f32_, f32_, f32_, u64, u64, i64, i32, i32, P, P]
@@ -287,6 +290,28 @@ def vndf_sample_cap_reflect(wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, wo_x, wo
     _stream_call("vndf_sample_cap_reflect",
                  (wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, wo_x, wo_y, wo_z, pdf, weight),
                  _IN + ("wo_x", "wo_y", "wo_z", "pdf", "weight"), n, stream)
+
+
+def _philox_reflect_call(fn, seed, first_index, n, wo_x, wo_y, wo_z, pdf, weight, stream):
+    dev = None
+    ptrs = []
+    for t, nm in zip((wo_x, wo_y, wo_z, pdf, weight), ("wo_x", "wo_y", "wo_z", "pdf", "weight")):
+        if t is None:
+            raise ValueError(f"{nm}: required")
+        p, dev = _dev_ptr(t, n, nm, device=dev)
+        ptrs.append(p)
+    _check(fn, getattr(lib(), fn)(int(seed), int(first_index), int(n), *ptrs, _stream(stream, dev)))
+
+
+def vndf_sample_cap_reflect_philox(seed, first_index, n, wo_x, wo_y, wo_z, pdf, weight, stream=None):
+    """NEXT-2 fused: config-4 inputs in-kernel, reflected direction, Eq. 20 pdf, G2/G1 weight."""
+    _philox_reflect_call("vndf_sample_cap_reflect_philox", seed, first_index, n, wo_x, wo_y, wo_z, pdf,
+                         weight, stream)
+
+
+def vndf_sample_heitz2018_reflect_philox(seed, first_index, n, wo_x, wo_y, wo_z, pdf, weight, stream=None):
+    _philox_reflect_call("vndf_sample_heitz2018_reflect_philox", seed, first_index, n, wo_x, wo_y, wo_z, pdf,
+                         weight, stream)
 
 
 def vndf_pdf(h_x, h_y, h_z, wi_x, wi_y, wi_z, alpha_x, alpha_y, pdf, n=None, stream=None):

@@ -134,6 +134,101 @@ __global__ void __launch_bounds__(PhiloxLaunch<METHOD>::kBlock, 1) philox_kernel
     }
 }
 
+// ------------------------------------------- fused Philox reflection (NEXT-2) --
+// Config-4 inputs generated in-kernel, then appendix steps (1)-(2):
+// wo = reflect(wi, h), the Eq. 20 pdf and the G2/G1 weight; 20 B written per
+// sample.  The cap kernel defers its ill-conditioned samples to the same
+// global queue + float64 fix-up kernel as philox_kernel.
+struct ReflectOut {
+    float *ox, *oy, *oz, *pdf, *weight;
+};
+
+template <int METHOD>
+__device__ __forceinline__ Reflected philox_reflect_one(const PhiloxKeys& ks, uint64_t ctr, uint64_t k,
+                                                        const FixQueue& fq, const float* __restrict__ tab) {
+    const Inputs in = c4_inputs_fp32<true, METHOD == kCap>(philox_sample_ks(ks, ctr), tab);
+    Reflected r;
+    if (METHOD == kCap) {
+        const bool flag = cap_reflect_fp32<false>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, r);
+        if (__builtin_expect(flag, 0)) {
+            const unsigned long long slot = atomicAdd(fq.count, 1ull);
+            if (slot < fq.cap) fq.idx[slot] = k;
+        }
+    } else {
+        heitz_reflect_fp32<false>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, r);
+    }
+    return r;
+}
+
+template <int METHOD, int V, bool ALIGNED>
+__global__ void __launch_bounds__(PhiloxLaunch<METHOD>::kBlock, 1)
+    philox_reflect_kernel(uint64_t first, int64_t n, ReflectOut out, FixQueue fq, const float* __restrict__ gtab,
+                          const __grid_constant__ PhiloxKeys ks) {
+    extern __shared__ __align__(16) float tab[];
+    __shared__ __align__(8) uint64_t tab_bar;
+    bulk_load_shared(tab, gtab, kSinTableBytes, &tab_bar);
+    const int64_t nchunks = n / V;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int64_t c = tid; c < nchunks; c += stride) {
+        const int64_t i = c * V;
+        const uint64_t base = first + (uint64_t)i;
+        Vec<V> ox, oy, oz, pd, wg;
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            const uint64_t ctr = ALIGNED ? (base | (uint64_t)j) : base + (uint64_t)j;
+            const Reflected r = philox_reflect_one<METHOD>(ks, ctr, (uint64_t)(i + j), fq, tab);
+            ox.v[j] = r.x;
+            oy.v[j] = r.y;
+            oz.v[j] = r.z;
+            pd.v[j] = r.pdf;
+            wg.v[j] = r.weight;
+        }
+        st_stream<V>(out.ox + i, ox);
+        st_stream<V>(out.oy + i, oy);
+        st_stream<V>(out.oz + i, oz);
+        st_stream<V>(out.pdf + i, pd);
+        st_stream<V>(out.weight + i, wg);
+    }
+    if (V > 1) {
+        const int64_t i = nchunks * V + tid;
+        if (i < n) {
+            const Reflected r = philox_reflect_one<METHOD>(ks, first + (uint64_t)i, (uint64_t)i, fq, tab);
+            out.ox[i] = r.x;
+            out.oy[i] = r.y;
+            out.oz[i] = r.z;
+            out.pdf[i] = r.pdf;
+            out.weight[i] = r.weight;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(128) philox_reflect_fixup_kernel(uint64_t seed, uint64_t first, int64_t n,
+                                                                    FixQueue fq, const float* __restrict__ gtab,
+                                                                    ReflectOut out) {
+    const uint64_t count = *fq.count;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    auto fix = [&](uint64_t k) {
+        double r[5];
+        cap_reflect_philox_fp64(seed, first + k, r);
+        out.ox[k] = (float)r[0];
+        out.oy[k] = (float)r[1];
+        out.oz[k] = (float)r[2];
+        out.pdf[k] = (float)r[3];
+        out.weight[k] = (float)r[4];
+    };
+    if (count <= fq.cap) {
+        for (uint64_t t = t0; t < count; t += stride) fix(fq.idx[t]);
+        return;
+    }
+    for (uint64_t k = t0; k < (uint64_t)n; k += stride) {  // overflow: rescan
+        const Inputs in = c4_inputs_fp32(philox_sample(seed, first + k), gtab);
+        Reflected r;
+        if (cap_reflect_fp32<false>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, r)) fix(k);
+    }
+}
+
 __global__ void __launch_bounds__(256) philox_words_kernel(uint64_t seed, uint64_t first, int64_t n,
                                                            uint32_t block, uint4* __restrict__ out) {
     const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));

@@ -399,6 +399,80 @@ vndf_status launch_philox(uint64_t seed, uint64_t first, int64_t n, float* hx, f
               : launch_philox_v<METHOD, false, PV, false>(seed, first, n, hx, hy, hz, pdf, s);
 }
 
+// Fused Philox reflection (NEXT-2): same grid, table, queue and fix-up
+// structure as launch_philox_v, five output planes.
+template <int METHOD, int V, bool ALIGNED>
+vndf_status launch_philox_reflect_v(uint64_t seed, uint64_t first, int64_t n, const ReflectOut& out,
+                                    cudaStream_t s) {
+    const void* k = (const void*)philox_reflect_kernel<METHOD, V, ALIGNED>;
+    const int block = block_size(PhiloxLaunch<METHOD>::kBlock);
+    const size_t smem = kSinTableBytes;
+    cudaError_t e = allow_dynamic_smem(k, smem);
+    if (e != cudaSuccess) return cuda_fail(e);
+    int grid = 0;
+    e = grid_for(k, block, std::max<int64_t>(n / V, 1), &grid, true, smem);
+    if (e != cudaSuccess) return cuda_fail(e);
+    FixQueue fq{nullptr, nullptr, 0};
+    void* qbuf = nullptr;
+    if (METHOD == kCap) {
+        fq.cap = (uint64_t)std::min<int64_t>(std::max<int64_t>(n / 128, 1 << 16), (int64_t)1 << 26);
+        e = queue_alloc(&qbuf, sizeof(unsigned long long) + fq.cap * sizeof(uint64_t), s);
+        if (e != cudaSuccess) return cuda_fail(e);
+        fq.count = (unsigned long long*)qbuf;
+        fq.idx = (uint64_t*)((char*)qbuf + sizeof(unsigned long long));
+        e = cudaMemsetAsync(fq.count, 0, sizeof(unsigned long long), s);
+        if (e != cudaSuccess) {
+            cudaFreeAsync(qbuf, s);
+            return cuda_fail(e);
+        }
+    }
+    float* gtab = nullptr;
+    e = sincos_table(&gtab);
+    if (e != cudaSuccess) {
+        if (qbuf) cudaFreeAsync(qbuf, s);
+        return cuda_fail(e);
+    }
+    philox_reflect_kernel<METHOD, V, ALIGNED><<<grid, block, smem, s>>>(first, n, out, fq, gtab, philox_keys(seed));
+    e = cudaGetLastError();
+    if (e == cudaSuccess && METHOD == kCap) {
+        int sms = 0;
+        e = sm_count(&sms);
+        const int64_t fix_blocks = std::min<int64_t>(((int64_t)fq.cap + 127) / 128, (int64_t)std::max(sms, 1) * 32);
+        if (e == cudaSuccess) {
+            philox_reflect_fixup_kernel<<<(int)fix_blocks, 128, 0, s>>>(seed, first, n, fq, gtab, out);
+            e = cudaGetLastError();
+        }
+    }
+    if (qbuf) {
+        const cudaError_t ef = cudaFreeAsync(qbuf, s);
+        if (e == cudaSuccess) e = ef;
+    }
+    return e == cudaSuccess ? VNDF_OK : cuda_fail(e);
+}
+
+template <int METHOD>
+vndf_status launch_philox_reflect(uint64_t seed, uint64_t first, int64_t n, float* ox, float* oy, float* oz,
+                                  float* pdf, float* weight, cudaStream_t s) {
+    if (n < 0) return VNDF_ERR_INVALID_ARGUMENT;
+    float* o[5] = {ox, oy, oz, pdf, weight};
+    for (auto p : o)
+        if (!p || !aligned(p, 4)) return VNDF_ERR_INVALID_ARGUMENT;
+    const int64_t bytes = n * (int64_t)sizeof(float);
+    if (n > 0)
+        for (int k = 0; k < 5; ++k)
+            for (int l = k + 1; l < 5; ++l)
+                if (overlaps(o[k], o[l], bytes)) return VNDF_ERR_INVALID_ARGUMENT;
+    if (n == 0) return VNDF_OK;
+    constexpr int PV = PhiloxLaunch<METHOD>::kV;
+    bool vec = true;
+    for (auto p : o) vec = vec && aligned(p, 4 * PV);
+    if (prefs().vector_width == 1) vec = false;
+    const ReflectOut out{ox, oy, oz, pdf, weight};
+    if (!vec) return launch_philox_reflect_v<METHOD, 1, true>(seed, first, n, out, s);
+    return first % PV == 0 ? launch_philox_reflect_v<METHOD, PV, true>(seed, first, n, out, s)
+                           : launch_philox_reflect_v<METHOD, PV, false>(seed, first, n, out, s);
+}
+
 // ------------------------------------------------ host-path staging cache --
 // Pageable host buffers: the blocking host entry point streams a batch through
 // device staging sets of kStagingChunk samples (11 planes each: 7 in, 4 out),
@@ -735,6 +809,19 @@ vndf_status vndf_sample_cap_reflect(const float* wi_x, const float* wi_y, const 
     }
     if (e == cudaSuccess) e = cudaGetLastError();
     return e == cudaSuccess ? VNDF_OK : cuda_fail(e);
+}
+
+vndf_status vndf_sample_cap_reflect_philox(uint64_t seed, uint64_t first_index, int64_t n, float* wo_x,
+                                           float* wo_y, float* wo_z, float* pdf, float* weight,
+                                           vndf_stream_t stream) {
+    return launch_philox_reflect<kCap>(seed, first_index, n, wo_x, wo_y, wo_z, pdf, weight, (cudaStream_t)stream);
+}
+
+vndf_status vndf_sample_heitz2018_reflect_philox(uint64_t seed, uint64_t first_index, int64_t n, float* wo_x,
+                                                 float* wo_y, float* wo_z, float* pdf, float* weight,
+                                                 vndf_stream_t stream) {
+    return launch_philox_reflect<kHeitz>(seed, first_index, n, wo_x, wo_y, wo_z, pdf, weight,
+                                         (cudaStream_t)stream);
 }
 
 vndf_status vndf_pdf(const float* h_x, const float* h_y, const float* h_z, const float* wi_x,

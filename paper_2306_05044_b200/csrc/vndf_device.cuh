@@ -608,18 +608,36 @@ __device__ __forceinline__ Inputs c4_inputs_fp32(uint4 W, const float* __restric
 
 __device__ __forceinline__ double u01d(uint32_t w) { return (double)(w >> 8) * 0x1p-24; }
 
-// Float64 fix-up for a config-4 sample: regenerate the word, build the inputs
-// in double from the exact uniforms, sample in double.
-__device__ __noinline__ float4 cap_philox_fp64(uint64_t seed, uint64_t i) {
-    const uint4 W = philox_sample(seed, i);
+// The config-4 inputs of a Philox block in double from the exact uniforms:
+// in = (wi.x, wi.y, wi.z, alpha_x, alpha_y, u1, u2) (vndf.h recipe).
+__device__ __forceinline__ void c4_inputs_fp64(uint4 W, double in[7]) {
     const double ua = (double)((W.x & 0xFFu) | ((W.y & 0xFFu) << 8)) * 0x1p-16;
     const double ub = (double)((W.z & 0xFFu) | ((W.w & 0xFFu) << 8)) * 0x1p-16;
     const double r = sqrt(ua * (2.0 - ua));
     double sp, cp;
     sincospi(2.0 * ub, &sp, &cp);
-    const double ax = exp2((u01d(W.z) - 1.0) * kLog2_100D);
-    const double ay = exp2((u01d(W.w) - 1.0) * kLog2_100D);
-    return cap_fp64_d(r * cp, r * sp, 1.0 - ua, ax, ay, u01d(W.x), u01d(W.y));
+    in[0] = r * cp;
+    in[1] = r * sp;
+    in[2] = 1.0 - ua;
+    in[3] = exp2((u01d(W.z) - 1.0) * kLog2_100D);
+    in[4] = exp2((u01d(W.w) - 1.0) * kLog2_100D);
+    in[5] = u01d(W.x);
+    in[6] = u01d(W.y);
+}
+
+// Float64 fix-up for a config-4 sample: regenerate the word, build the inputs
+// in double from the exact uniforms, sample in double.
+__device__ __noinline__ float4 cap_philox_fp64(uint64_t seed, uint64_t i) {
+    double in[7];
+    c4_inputs_fp64(philox_sample(seed, i), in);
+    return cap_fp64_d(in[0], in[1], in[2], in[3], in[4], in[5], in[6]);
+}
+
+// The same for the reflection outputs (wo.xyz, Eq. 20 pdf, G2/G1 weight).
+__device__ __noinline__ void cap_reflect_philox_fp64(uint64_t seed, uint64_t i, double out[5]) {
+    double in[7];
+    c4_inputs_fp64(philox_sample(seed, i), in);
+    cap_reflect_fp64_d(in[0], in[1], in[2], in[3], in[4], in[5], in[6], out);
 }
 
 }  // namespace vndf

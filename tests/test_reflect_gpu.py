@@ -98,3 +98,77 @@ def test_reflect_gpu_distribution_eq20(env, theta, alpha):
         wo = np.stack([o.cpu().numpy() for o in out[:3]]).astype(np.float64)
         passes.append(stats.pearson(stats.sphere_histogram(wo), masses)[2] > 1e-3)
     assert sum(passes) >= 2, passes
+
+
+def _reflect_errors(got, ref):
+    ewo = np.abs(got[:3] - ref[:3]).max(axis=0)
+    epdf = np.abs(got[3] - ref[3]) / ref[3]
+    ew = np.abs(got[4] - ref[4])
+    return ewo, epdf, ew
+
+
+@pytest.mark.parametrize("first,n", [(0, (1 << 20) + 3), ((1 << 32) - 4097, 8192 + 5)])
+def test_reflect_philox_parity(env, first, n):
+    """Fused Philox reflection (config-4 inputs generated in-kernel): every
+    sample against the oracle's orc_sample_reflect on orc_c4_inputs, across
+    aligned / unaligned first_index and the 32-bit counter carry."""
+    oracle, vndf, synth, dev = env
+    out = [torch.empty(n, dtype=torch.float32, device=dev) for _ in range(5)]
+    vndf.vndf_sample_cap_reflect_philox(3, first, n, *out)
+    torch.cuda.synchronize()
+    ref = oracle.batch_sample_reflect_philox(oracle.CAP, 3, np.arange(first, first + n, dtype=np.uint64))
+    got = np.stack([o.cpu().numpy() for o in out]).astype(np.float64)
+    ewo, epdf, ew = _reflect_errors(got, ref)
+    print(f"philox reflect first={first}: max |dwo| {ewo.max():.2e}, pdf rel {epdf.max():.2e}, "
+          f"|dweight| {ew.max():.2e}")
+    assert ewo.max() <= TOL_WO and epdf.max() <= TOL_PDF and ew.max() <= TOL_W
+    assert np.abs(np.linalg.norm(got[:3], axis=0) - 1).max() < 1e-5
+
+
+def test_reflect_philox_full_size_sampled(env):
+    """2^28 samples in one call (the bench size), 2^20 sampled indices plus the
+    ends compared one by one; and the fused outputs equal the streamed kernel's
+    on the same (fp32-rounded) inputs within the contract."""
+    oracle, vndf, synth, dev = env
+    n = 1 << 28
+    out = [torch.empty(n, dtype=torch.float32, device=dev) for _ in range(5)]
+    vndf.vndf_sample_cap_reflect_philox(3, 0, n, *out)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(28)
+    idx = np.unique(np.concatenate([rng.integers(0, n, 1 << 20), np.arange(2048), np.arange(n - 2048, n)]))
+    ti = torch.from_numpy(idx).to(dev)
+    ref = oracle.batch_sample_reflect_philox(oracle.CAP, 3, idx.astype(np.uint64))
+    got = np.stack([o[ti].cpu().numpy() for o in out]).astype(np.float64)
+    ewo, epdf, ew = _reflect_errors(got, ref)
+    assert ewo.max() <= TOL_WO and epdf.max() <= TOL_PDF and ew.max() <= TOL_W
+    assert bool(torch.isfinite(out[3]).all()) and float(out[3].min()) > 0
+    assert float(out[4].min()) >= 0.0 and float(out[4].max()) <= 1.0 + 1e-6
+    del out
+    torch.cuda.empty_cache()
+
+
+def test_reflect_philox_offsets_and_heitz(env):
+    """first_index offsets are bit-identical to slices of a first_index = 0
+    call (cap and Heitz); the Heitz baseline (literal fp32, no fix-up) meets
+    the contract on >= 98% of samples and keeps unit directions."""
+    oracle, vndf, synth, dev = env
+    n = (1 << 16) + 3
+    for fn in (vndf.vndf_sample_cap_reflect_philox, vndf.vndf_sample_heitz2018_reflect_philox):
+        ref = [torch.empty(n + 8, dtype=torch.float32, device=dev) for _ in range(5)]
+        fn(11, 0, n + 8, *ref)
+        for f in (1, 3, 4, 6):
+            out = [torch.empty(n, dtype=torch.float32, device=dev) for _ in range(5)]
+            fn(11, f, n, *out)
+            torch.cuda.synchronize()
+            for u, v in zip(out, ref):
+                assert torch.equal(u, v[f:f + n]), (fn.__name__, f)
+    out = [torch.empty(n, dtype=torch.float32, device=dev) for _ in range(5)]
+    vndf.vndf_sample_heitz2018_reflect_philox(11, 0, n, *out)
+    torch.cuda.synchronize()
+    ref = oracle.batch_sample_reflect_philox(oracle.HEITZ, 11, np.arange(n, dtype=np.uint64))
+    got = np.stack([o.cpu().numpy() for o in out]).astype(np.float64)
+    ewo, epdf, ew = _reflect_errors(got, ref)
+    ok = (ewo <= TOL_WO) & (epdf <= TOL_PDF) & (ew <= TOL_W)
+    print(f"heitz philox reflect: within contract on {ok.mean():.5f} of samples")
+    assert ok.mean() >= 0.98
+    assert np.abs(np.linalg.norm(got[:3], axis=0) - 1).max() < 1e-4

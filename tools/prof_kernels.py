@@ -38,6 +38,13 @@ if which in ("all", "c4"):
         vndf.vndf_sample_cap_philox(3, 0, n, *o)
         vndf.vndf_sample_heitz2018_philox(3, 0, n, *o)
     torch.cuda.synchronize()
+if which in ("all", "reflect_philox"):
+    n = 1 << 26
+    o = [torch.empty(n, device=dev) for _ in range(5)]
+    for _ in range(2):
+        vndf.vndf_sample_cap_reflect_philox(3, 0, n, *o)
+        vndf.vndf_sample_heitz2018_reflect_philox(3, 0, n, *o)
+    torch.cuda.synchronize()
 print("ok")
 
 if which in ("all", "next"):
