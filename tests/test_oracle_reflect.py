@@ -137,3 +137,15 @@ def test_reflected_directions_follow_eq20(orc, method, theta, alpha):
     assert masses.sum() == pytest.approx(1.0, abs=2e-3)
     _, _, pv = stats.pearson(stats.sphere_histogram(out[:3]), masses)
     assert pv > 1e-3, pv
+
+
+def test_batch_reflect_philox_driver(orc):
+    """The Philox batch driver is orc_sample_reflect on orc_c4_inputs, index by
+    index (no arithmetic of its own), for both methods and 64-bit indices."""
+    idx = np.array([0, 1, 7, 4095, (1 << 32) - 1, 1 << 32, (1 << 40) + 3], dtype=np.uint64)
+    for method in (orc.CAP, orc.HEITZ):
+        got = orc.batch_sample_reflect_philox(method, 9, idx, threads=3)
+        for k, i in enumerate(idx):
+            x = orc.c4_inputs(9, int(i))
+            want = orc.sample_reflect(method, x[:3], x[3], x[4], x[5], x[6])
+            np.testing.assert_array_equal(got[:, k], want)
