@@ -1,5 +1,6 @@
-// kernels_philox.cuh -- fused Philox4x32-10 kernels (config 4), the deferred fix-up queue
-// and kernel, raw Philox words, fix-up counters.
+// kernels_philox.cuh -- fused Philox4x32-10 kernels (config 4) and their fused
+// reflection twins (NEXT-2), the deferred fix-up queues and kernels, raw Philox
+// words, fix-up counters.
 // Part of libvndf's single translation unit (included by vndf.cu inside its
 // anonymous namespace); see vndf.cu for the kernel list and DESIGN.md s.6.
 #pragma once

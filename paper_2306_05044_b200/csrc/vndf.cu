@@ -11,15 +11,18 @@
 //   kernels_stream.cuh   stream_kernel<METHOD, PDF, V>: streamed SoA sampling
 //                        (cap, Heitz, native cap), one V-sample chunk per
 //                        thread, block-level float64 fix-up queue
-//   kernels_philox.cuh   philox_kernel<METHOD, PDF, V>: fused Philox4x32-10
-//                        generation + sampling + pdf, deferred fix-up queue and
-//                        kernel; raw Philox words; fix-up counters
+//   kernels_philox.cuh   philox_kernel<METHOD, PDF, V, ALIGNED>: fused
+//                        Philox4x32-10 generation + sampling + pdf;
+//                        philox_reflect_kernel: the same + reflection, Eq. 20
+//                        pdf and G2/G1 weight (NEXT-2); deferred fix-up queues
+//                        and kernels; raw Philox words; fix-up counters
 //   kernels_next.cuh     pdf_kernel (NEXT-4), reflect_kernel / furnace_kernel
 //                        (NEXT-2), histogram_kernel (NEXT-3), microbench_kernel
 //                        (NEXT-1)
 //   vndf.cu (this file)  launch configuration, argument validation, device
-//                        caches (occupancy, sin/cos table, memory pool, host
-//                        staging), the extern "C" entry points
+//                        caches (occupancy, sine table, memory pool, host
+//                        staging), the zero-copy host path, the extern "C"
+//                        entry points
 #include <cuda_runtime.h>
 
 #include <algorithm>
