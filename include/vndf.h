@@ -41,9 +41,13 @@
  *   - Calls only ENQUEUE work on `stream` (NULL = legacy default stream) and
  *     return; outputs are valid once the caller synchronises the stream.
  *     The *_host call is the exception: it is blocking.
+ *   - The device calls can be captured into a CUDA graph (stream capture) once
+ *     the device's global state exists, i.e. after one call of the same kind
+ *     on that device outside capture (the first fused call uploads the sine
+ *     table synchronously).  Replays recompute from the captured buffers.
  *   - Thread-safe.  Global state, per device, created on first use and kept
  *     for the life of the process: cached device attributes and launch
- *     configurations, a 64 KB sin/cos table (fused Philox path), a private
+ *     configurations, a 64 KB sine table (fused Philox path), a private
  *     stream-ordered memory pool for transient fix-up queues, and the host
  *     entry point's staging area (see vndf_release_host_staging).
  *   - Outputs are a pure function of the inputs (of seed and global index for
