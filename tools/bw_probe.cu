@@ -70,7 +70,33 @@ double run(long n, const float* const* din, float* const* dout, int blocks_per_s
     return (double)(R + W) * 4.0 * n / (ms / reps * 1e-3) / 1e9;
 }
 
-int main() {
+int main(int argc, char** argv) {
+    // mode "stagger": planes carved from one slab with a per-plane stagger
+    if (argc > 1 && std::string(argv[1]) == "stagger") {
+        for (long n : {1L << 24, 1L << 26}) {
+            for (long stagger : {0L, 256L, 4096L, 65536L, 1L << 20, 3L << 20}) {
+                float* slab = nullptr;
+                const size_t plane = n * sizeof(float) + stagger;
+                cudaMalloc(&slab, 12 * plane + 4096);
+                cudaMemset(slab, 0, 12 * plane + 4096);
+                const float** din;
+                float** dout;
+                cudaMallocManaged(&din, 8 * sizeof(float*));
+                cudaMallocManaged(&dout, 4 * sizeof(float*));
+                char* base = (char*)slab;
+                for (int k = 0; k < 8; ++k) din[k] = (const float*)(base + k * plane);
+                for (int k = 0; k < 4; ++k) dout[k] = (float*)(base + (8 + k) * plane);
+                cudaDeviceSynchronize();
+                printf("n=2^%d stagger %8ld B: (7,4) %5.0f  (7,3) %5.0f  (8,4) %5.0f GB/s\n", n == (1L << 24) ? 24 : 26,
+                       stagger, run<7, 4>(n, din, dout, 0), run<7, 3>(n, din, dout, 0), run<8, 4>(n, din, dout, 0));
+                cudaFree(slab);
+                cudaFree(din);
+                cudaFree(dout);
+            }
+        }
+        return 0;
+    }
+
     for (long n : {1L << 24, 1L << 26}) {
         // one allocation per plane of exactly n floats, as torch.empty would make them
         std::vector<float*> bufs(12);
