@@ -243,7 +243,10 @@ def roofline(bytes_per_launch: float, launch_ms: float, kernel_key: str):
             "algorithmic_bytes_per_launch": int(bytes_per_launch),
             # context only: the HGX B200 HBM3e figure (B200_PROFILING.md); the
             # measured copy above is the denominator
-            "spec_gbs": 7700.0, "frac_of_spec": round(achieved / 7700.0, 4)}
+            "spec_gbs": 7700.0, "frac_of_spec": round(achieved / 7700.0, 4),
+            # context: the same 7-read / 4-write plane pattern with no arithmetic
+            # (tools/bw_probe.cu, profiles/r1/pattern_probes_r1.txt)
+            "pattern_probe_gbs": _traffic_entry("pattern_probe_7r4w_2e24_gbs")}
 
 
 def _traffic_entry(key: str):
