@@ -122,3 +122,53 @@ def test_garbage_inputs_never_trap(env):
     h_ref, p_ref, _ = oracle.batch_sample(oracle.CAP, *[x[k].cpu().numpy() for k in synth.PLANES])
     h = np.stack([t.cpu().numpy() for t in o[:3]]).astype(np.float64)
     assert np.abs(h - h_ref).max() <= TOL_H
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_whole_domain_random(env, seed):
+    """vndf.h's whole per-sample domain at once: wi uniform over the sphere
+    (both hemispheres, grazing included) with |wi| log-uniform in [0.5, 2],
+    alpha_x, alpha_y independently log-uniform in [1e-3, 1], u1, u2 uniform on
+    the fp32 grid of [0, 1); 2^22 samples, every one against the oracle."""
+    oracle, vndf, synth, dev = env
+    n = 1 << 22
+    g = torch.Generator(device="cpu").manual_seed(1234 + seed)
+    d = torch.randn(3, n, generator=g, dtype=torch.float64)
+    d /= d.norm(dim=0, keepdim=True)
+    mag = torch.exp(torch.empty(n, dtype=torch.float64).uniform_(np.log(0.5), np.log(2.0), generator=g))
+    w = (d * mag).float()
+    a = torch.exp(torch.empty(2, n, dtype=torch.float64).uniform_(np.log(1e-3), 0.0, generator=g)).float()
+    u = (torch.randint(0, 1 << 24, (2, n), generator=g).double() * 2.0**-24).float()
+    planes = [w[0], w[1], w[2], a[0], a[1], u[0], u[1]]
+    t = [p.contiguous().to(dev) for p in planes]
+    out = vndf.empty_outputs(n, dev)
+    vndf.vndf_sample_cap_pdf(*t, *out)
+    torch.cuda.synchronize()
+    h_ref, p_ref, _ = oracle.batch_sample(oracle.CAP, *[p.numpy() for p in planes])
+    h = np.stack([o.cpu().numpy() for o in out[:3]]).astype(np.float64)
+    p = out[3].cpu().numpy().astype(np.float64)
+    eh = np.abs(h - h_ref).max()
+    ep = (np.abs(p - p_ref) / p_ref).max()
+    print(f"whole domain seed {seed}: max |dh| {eh:.2e}, pdf rel {ep:.2e}")
+    assert eh <= TOL_H and ep <= TOL_PDF
+    # the paper's native below-horizon handling (NEXT-3) on the same inputs
+    vndf.vndf_sample_cap_pdf_native(*t, *out)
+    torch.cuda.synchronize()
+    m = 1 << 19  # the native oracle runs binary128 (reading R17): a 2^19 prefix
+    h_ref, p_ref = oracle.batch_sample_native(oracle.CAP, *[p[:m].numpy() for p in planes])
+    h = np.stack([o[:m].cpu().numpy() for o in out[:3]]).astype(np.float64)
+    p = out[3][:m].cpu().numpy().astype(np.float64)
+    eh, ep = np.abs(h - h_ref).max(), (np.abs(p - p_ref) / p_ref).max()
+    print(f"  native: max |dh| {eh:.2e}, pdf rel {ep:.2e}")
+    assert eh <= TOL_H and ep <= TOL_PDF
+    # reflection (NEXT-2; tolerances of DESIGN.md s.6.5)
+    ro = [torch.empty(n, dtype=torch.float32, device=dev) for _ in range(5)]
+    vndf.vndf_sample_cap_reflect(*t, *ro)
+    torch.cuda.synchronize()
+    ref = oracle.batch_sample_reflect(oracle.CAP, *[p.numpy() for p in planes])
+    got = np.stack([o.cpu().numpy() for o in ro]).astype(np.float64)
+    ewo = np.abs(got[:3] - ref[:3]).max()
+    epd = (np.abs(got[3] - ref[3]) / ref[3]).max()
+    ewt = np.abs(got[4] - ref[4]).max()
+    print(f"  reflect: max |dwo| {ewo:.2e}, pdf rel {epd:.2e}, |dweight| {ewt:.2e}")
+    assert ewo <= 6e-5 and epd <= 1e-4 and ewt <= 1e-4
