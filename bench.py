@@ -380,6 +380,36 @@ def variants(torch, vndf, synth, dev, stream, x2, out2):
     res["c2_cap_pdf"] = {"gsamples_s": n2 / t_cap / 1e6, "ms": t_cap}
     res["c2_heitz_pdf"] = {"gsamples_s": n2 / t_hz / 1e6, "ms": t_hz, "t_heitz_over_t_cap": t_hz / t_cap}
 
+    # config 1: 2^16 samples, L2-resident and launch-bound (report
+    # us per launch): 50 launches captured in one CUDA graph, replayed, so the
+    # device time per launch is measured without the host's per-call cost
+    c1 = synth.CONFIGS[1]
+    x1 = synth.fill(c1.recipe, c1.seed, c1.n, device=dev)
+    o1 = vndf.empty_outputs(c1.n, dev)
+    ins1 = [x1[k] for k in synth.PLANES]
+    vndf.vndf_sample_cap_pdf(*ins1, *o1)
+    vndf.vndf_sample_heitz2018(*ins1, *o1)
+    torch.cuda.synchronize()
+    c1res = {}
+    for name, fn in (("cap", vndf.vndf_sample_cap_pdf), ("heitz", vndf.vndf_sample_heitz2018)):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(50):
+                fn(*ins1, *o1)
+        g.replay()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        for _ in range(10):
+            g.replay()
+        ev1.record()
+        torch.cuda.synchronize()
+        us = ev0.elapsed_time(ev1) * 1e3 / 500
+        c1res[name] = {"us_per_launch": us, "gsamples_s": c1.n / us / 1e3}
+    c1res["t_heitz_over_t_cap"] = c1res["heitz"]["us_per_launch"] / c1res["cap"]["us_per_launch"]
+    res["c1_latency"] = c1res
+    del x1, o1, ins1
+
     # config 3: 2^28 streamed, h only
     c3 = synth.CONFIGS[3]
     x3 = synth.fill(c3.recipe, c3.seed, c3.n, device=dev)
