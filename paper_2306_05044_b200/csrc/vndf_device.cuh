@@ -222,49 +222,58 @@ __device__ __forceinline__ bool cap_reflect_fp32(float wx, float wy, float wz, f
 
 // ---------------------------------------------------------------------------
 // Float64 recomputation of one cap sample (the fix-up).  Same algebra as
-// cap_fp32, IEEE double throughout (sincospi, sqrt, division).
+// cap_fp32, in double throughout (sincospi, sqrt, rsqrt, division).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ float4 cap_fp64_d(double wx, double wy, double wz, double ax, double ay,
                                              double u1, double u2, bool flip = true) {
+    // Normalisations by rsqrt (61 cycles dependent) instead of sqrt + divide
+    // (151): the recomputation's latency is what a one-wave launch exposes.
+    // rsqrt is ~1 ulp in double, far below the 1e-9 this path needs.
     const double s = (flip && wz < 0.0) ? -1.0 : 1.0;
     const double tx = ax * wx, ty = ay * wy;
-    const double L = sqrt(tx * tx + ty * ty + wz * wz);
-    const double wsx = s * tx / L, wsy = s * ty / L, wsz = s * wz / L;
-    const double a = 1.0 + wsz;
+    const double iL = s * rsqrt(tx * tx + ty * ty + wz * wz);
+    const double wsx = tx * iL, wsy = ty * iL, wsz = wz * iL;
+    const double rs2 = wsx * wsx + wsy * wsy;
+    double a;  // 1 + ws.z; native frame below the horizon: rs^2 / (1 - ws.z), no cancellation
+    if (!flip && wsz < 0.0)
+        a = rs2 / (1.0 - wsz);
+    else
+        a = 1.0 + wsz;
     const double q = 1.0 - u2;
     const double hz = q * a;
-    const double rs2 = wsx * wsx + wsy * wsy;
     const double st = sqrt(u2 * (hz * a + rs2));
     double sp, cp;
     sincospi(2.0 * u1, &sp, &cp);
-    const double hx = st * cp + wsx, hy = st * sp + wsy;
+    const double hx = fma(st, cp, wsx), hy = fma(st, sp, wsy);
     const double mx = ax * hx, my = ay * hy;
     const double m2 = mx * mx + my * my + hz * hz;
-    const double N = sqrt(m2);
+    const double iN = rsqrt(m2);
     const double hs2 = hx * hx + hy * hy + hz * hz;
-    const double pdf = m2 * N / (kPiD * ax * ay * a * hs2);
-    return make_float4((float)(s * mx / N), (float)(s * my / N), (float)(s * hz / N), (float)pdf);
+    const double pdf = m2 * m2 * iN / (kPiD * ax * ay * a * hs2);
+    const double t = s * iN;
+    return make_float4((float)(mx * t), (float)(my * t), (float)(hz * t), (float)pdf);
 }
 
 // Float64 reflection sample (fix-up of cap_reflect_fp32), same formulas.
 __device__ __forceinline__ void cap_reflect_fp64_d(double wx, double wy, double wz, double ax, double ay,
                                                    double u1, double u2, double out[5]) {
     const double s = (wz < 0.0) ? -1.0 : 1.0;
-    const double nw = sqrt(wx * wx + wy * wy + wz * wz);
-    const double ux = s * wx / nw, uy = s * wy / nw, uz = s * wz / nw;   // w'
+    const double inw = s * rsqrt(wx * wx + wy * wy + wz * wz);
+    const double ux = wx * inw, uy = wy * inw, uz = wz * inw;          // w'
     const double tx = ax * ux, ty = ay * uy;
-    const double L = sqrt(tx * tx + ty * ty + uz * uz);
-    const double wsx = tx / L, wsy = ty / L, wsz = uz / L;
+    const double L2 = tx * tx + ty * ty + uz * uz;
+    const double iL = rsqrt(L2), L = L2 * iL;
+    const double wsx = tx * iL, wsy = ty * iL, wsz = uz * iL;
     const double a = 1.0 + wsz, q = 1.0 - u2;
     const double hz = q * a;
     const double st = sqrt(u2 * (hz * a + wsx * wsx + wsy * wsy));
     double sp, cp;
     sincospi(2.0 * u1, &sp, &cp);
-    const double hx = st * cp + wsx, hy = st * sp + wsy;
+    const double hx = fma(st, cp, wsx), hy = fma(st, sp, wsy);
     const double mx = ax * hx, my = ay * hy;
-    const double m2 = mx * mx + my * my + hz * hz, N = sqrt(m2);
+    const double m2 = mx * mx + my * my + hz * hz, iN = rsqrt(m2);
     const double hs2 = hx * hx + hy * hy + hz * hz;
-    const double h0 = mx / N, h1 = my / N, h2 = hz / N;               // h' (upper frame)
+    const double h0 = mx * iN, h1 = my * iN, h2 = hz * iN;            // h' (upper frame)
     const double dot = ux * h0 + uy * h1 + uz * h2;
     const double ox = 2.0 * dot * h0 - ux, oy = 2.0 * dot * h1 - uy, oz = 2.0 * dot * h2 - uz;
     const double Lo = sqrt(ax * ax * ox * ox + ay * ay * oy * oy + oz * oz);
