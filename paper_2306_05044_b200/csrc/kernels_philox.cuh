@@ -5,6 +5,14 @@
 // anonymous namespace); see vndf.cu for the kernel list and DESIGN.md s.6.
 #pragma once
 
+// Uniform conversion of the cap kernel: 0 = SHF (ALU pipe), 1 = IMAD.HI shifts
+// (fw_hi, FMA-heavy pipe).  1 won with three 256-thread blocks per SM (ALU
+// pipe busier); with one 768-thread block per SM the FMA-heavy pipe is the
+// busier one and 0 is 2.5% faster (tools/variants.py).
+#ifndef VNDF_CAP_FW_HI
+#define VNDF_CAP_FW_HI 0
+#endif
+
 // ----------------------------------------------------- fused Philox kernel --
 // Deferred float64 fix-up queue of the fused kernel (compute-bound: inline
 // fp64 work would diverge the warp and its call would inflate the register
@@ -17,7 +25,7 @@
 template <int METHOD, bool PDF>
 __device__ __forceinline__ Sample philox_one(const PhiloxKeys& ks, uint64_t ctr, uint64_t k,
                                              const FixQueue& fq, const float* __restrict__ tab) {
-    const Inputs in = c4_inputs_fp32<true, METHOD == kCap>(philox_sample_ks(ks, ctr), tab);
+    const Inputs in = c4_inputs_fp32<true, VNDF_CAP_FW_HI && METHOD == kCap>(philox_sample_ks(ks, ctr), tab);
     Sample o;
     if (METHOD == kCap) {
         // config-4 inputs are on the upper hemisphere (wi.z = 1 - u > 0): no flip
@@ -147,7 +155,7 @@ struct ReflectOut {
 template <int METHOD>
 __device__ __forceinline__ Reflected philox_reflect_one(const PhiloxKeys& ks, uint64_t ctr, uint64_t k,
                                                         const FixQueue& fq, const float* __restrict__ tab) {
-    const Inputs in = c4_inputs_fp32<true, METHOD == kCap>(philox_sample_ks(ks, ctr), tab);
+    const Inputs in = c4_inputs_fp32<true, VNDF_CAP_FW_HI && METHOD == kCap>(philox_sample_ks(ks, ctr), tab);
     Reflected r;
     if (METHOD == kCap) {
         const bool flag = cap_reflect_fp32<false>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, r);

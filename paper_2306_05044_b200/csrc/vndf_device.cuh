@@ -509,8 +509,8 @@ __device__ __forceinline__ uint32_t imad_hi(uint32_t a, uint32_t b) {
 }
 
 __device__ __forceinline__ float fw(uint32_t w) { return __uint2float_rn(w >> 8); }
-// The same value with the shift as a high multiply (FMA pipe, see imad): the
-// fused cap kernel is short of ALU issue, the Heitz one of FMA issue.
+// The same value with the shift as a high multiply (FMA-heavy pipe, see imad),
+// for kernels short of ALU-pipe issue (VNDF_CAP_FW_HI).
 __device__ __forceinline__ float fw_hi(uint32_t w) { return __uint2float_rn(imad_hi(w, 1u << 24)); }
 template <bool HI>
 __device__ __forceinline__ float fw_t(uint32_t w) { return HI ? fw_hi(w) : fw(w); }
@@ -561,11 +561,19 @@ __device__ __forceinline__ uint4 philox_sample(uint64_t seed, uint64_t i) {
 // with r = K mod 2^14 and j = r (even quadrant) or 2^14 - r (odd quadrant),
 // sin = +-S[j], cos = +-S[2^14 - j]; the signs are the quadrant's, applied to
 // the sign bit.  Exact reduction, ~0.5 ulp: relative accuracy in each
-// component.  The index and sign arithmetic is IMAD-shaped (FMA pipe) and two
-// LDS.32 replace the octant table's swap selects: the fused kernel is short of
-// ALU-pipe issue slots (profiles/r1/prof_c4_r1_summary.txt).
+// component.  Two LDS.32 replace the octant table's four swap/sign selects; the
+// index and sign arithmetic can be pinned to IMAD (VNDF_TABLE_IMAD) for kernels
+// short of ALU-pipe issue (profiles/r1/prof_c4_r1_summary.txt).
 constexpr int kSinTableEntries = 16388;  // 16385 used, padded to a 16-byte multiple
 constexpr unsigned kSinTableBytes = kSinTableEntries * sizeof(float);
+// Index and sign arithmetic of the table lookup: 1 = pinned to IMAD (FMA-heavy
+// pipe), 0 = the compiler's SHF/IADD3/SEL (ALU pipe).  1 won with three
+// 256-thread blocks per SM; with one block per SM (FMA-heavy pipe the busier)
+// 0 is faster: cap +1.1%, Heitz +2.8% (tools/variants.py).
+#ifndef VNDF_TABLE_IMAD
+#define VNDF_TABLE_IMAD 0
+#endif
+
 // 2^16 as a constant-bank value: a literal power-of-two multiplier is
 // strength-reduced to SHF/IADD3 (ALU pipe) even through mad.lo.
 __constant__ uint32_t kImad2e16 = 65536u;
@@ -573,12 +581,19 @@ __constant__ uint32_t kImad2e16 = 65536u;
 __device__ __forceinline__ void sincos_2pi_u16(uint32_t K, const float* __restrict__ S, float* s,
                                                float* c) {
     const uint32_t r = K & 0x3FFFu;
+#if VNDF_TABLE_IMAD
     const uint32_t odd = imad_hi(K & 0x4000u, 1u << 18);        // bit 14 of K
     const uint32_t js = imad(odd, imad(r, 0xFFFFFFFEu, 16384u), r);  // r or 2^14 - r
     const float a = S[js], b = S[16384u - js];
     const uint32_t m16 = kImad2e16;
     *s = __uint_as_float(__float_as_uint(a) ^ (imad(K, m16, 0u) & 0x80000000u));           // q = 2, 3
     *c = __uint_as_float(__float_as_uint(b) ^ (imad(K, m16, 0x40000000u) & 0x80000000u));  // q = 1, 2
+#else
+    const uint32_t js = (K & 0x4000u) ? 16384u - r : r;  // r or 2^14 - r
+    const float a = S[js], b = S[16384u - js];
+    *s = __uint_as_float(__float_as_uint(a) ^ ((K << 16) & 0x80000000u));             // q = 2, 3
+    *c = __uint_as_float(__float_as_uint(b) ^ (((K + 0x4000u) << 16) & 0x80000000u));  // q = 1, 2
+#endif
 }
 
 // tab = nullptr: sincospif; else the 16-bit table (shared or global memory).
