@@ -73,20 +73,21 @@ __global__ void __launch_bounds__(128) philox_fixup_kernel(uint64_t seed, uint64
 }
 
 // One block per SM, holding the SM's single copy of the 64 KB table: the cap
-// kernel with 768 threads (24 warps, <= 85 registers), the Heitz kernel with
-// 1024 (32 warps, <= 64 registers).  Swept on B200 (tools/variants.py) over
-// 256 x 3, 320-512 x 2 and 640-1024 x 1 blocks per SM: cap 184 (256 x 3) ->
-// 190 Gsamples/s, Heitz 175 -> 178.
+// kernel with 640 threads (20 warps), the Heitz kernel with 1024 (32 warps,
+// <= 64 registers); both with 8 samples per thread (one 256-bit store per
+// output plane).  Swept on B200 (tools/build_variant.py + tools/variants.py)
+// over 256 x 3, 320-512 x 2 and 512-1024 x 1 blocks per SM and 2/4/8 samples
+// per thread: cap 184 (256 x 3, 4 per thread) -> 204 Gsamples/s, Heitz
+// 175 -> 186.5, together with the pipe-balance knobs VNDF_CAP_FW_HI and
+// VNDF_TABLE_IMAD.
 #ifndef VNDF_PHILOX_BLOCK_CAP
-#define VNDF_PHILOX_BLOCK_CAP 768
+#define VNDF_PHILOX_BLOCK_CAP 640
 #endif
 #ifndef VNDF_PHILOX_BLOCK_HEITZ
 #define VNDF_PHILOX_BLOCK_HEITZ 1024
 #endif
-// Samples per thread per chunk (one 128- or 256-bit store per output plane):
-// 4 for the cap (8: same speed), 8 for Heitz (+1.9% over 4).
 #ifndef VNDF_PHILOX_V_CAP
-#define VNDF_PHILOX_V_CAP 4
+#define VNDF_PHILOX_V_CAP 8
 #endif
 #ifndef VNDF_PHILOX_V_HEITZ
 #define VNDF_PHILOX_V_HEITZ 8
