@@ -365,9 +365,9 @@ def run_ours(args):
 
 def variants(torch, vndf, synth, dev, stream, x2, out2):
     """Side measurements on identical inputs (not the headline): Heitz-2018 on
-    config 2, configs 3/4/5 (cap and Heitz), each 3 warm-up + 10 timed launches."""
+    config 2, configs 3/4/5 (cap and Heitz), each 3 warm-up + 20 timed launches."""
     res = {}
-    reps, warm = 10, 3
+    reps, warm = 20, 3
 
     def timed(fn):
         total, per = time_launches(torch, fn, reps, warm, stream, per_step=False)
