@@ -259,6 +259,21 @@ def _traffic_entry(key: str):
         return None
 
 
+def mix_roofline(gsamples_s: float, sm_mhz: float = None):
+    """Tighter bound of the fused cap kernel (DESIGN.md s.6.4): its dynamic
+    instruction mix (ncu) weighted by dispatch cycles per instruction type
+    MEASURED on B200 (tools/pipe_probe.cu: 3-register LOP3 / IMAD.WIDE are
+    half rate), i.e. SMSP-cycles per 32 samples."""
+    cyc = _traffic_entry("cap_philox_c4_mix_cycles_per_warp_sample")
+    if not cyc:
+        return None
+    f = (sm_mhz or 1965.0) * 1e6
+    peak = 148 * 4 * f * 32 / cyc / 1e9
+    return {"achieved": round(gsamples_s, 2), "peak": round(peak, 2), "unit": "Gsamples/s",
+            "frac": round(gsamples_s / peak, 4),
+            "model": f"{cyc} dispatch cycles per 32 samples (measured per-type rates x ncu mix)"}
+
+
 def issue_roofline(gsamples_s: float, key: str, sm_mhz: float = None):
     """Instruction-issue bound of a compute-bound kernel (DESIGN.md s.6.4): each
     of the 4 SMSPs of the 148 SMs issues one warp-instruction per clock, so the
@@ -444,6 +459,7 @@ def variants(torch, vndf, synth, dev, stream, x2, out2):
     res["c4_cap_philox"] = {"gsamples_s": c4.n / t_cap4 / 1e6, "ms": t_cap4,
                             "write_gb_s": 16 * c4.n / t_cap4 / 1e6,
                             "roofline": issue_roofline(c4.n / t_cap4 / 1e6, "cap_philox_c4_warp_inst_per_sample"),
+                            "mix_bound": mix_roofline(c4.n / t_cap4 / 1e6),
                             "pipes_ncu": _traffic_entry("cap_philox_c4_pipes")}
     res["c4_heitz_philox"] = {"gsamples_s": c4.n / t_hz4 / 1e6, "ms": t_hz4,
                               "t_heitz_over_t_cap": t_hz4 / t_cap4,
