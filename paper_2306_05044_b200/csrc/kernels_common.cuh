@@ -28,6 +28,7 @@ struct StreamArgs {
     float* hy;
     float* hz;
     float* pdf;
+    int fix_cap;  // block fix-up queue slots used (<= kBlockFixCap; smaller only to test overflow)
 };
 
 // ---------------------------------------------------------------- memory ops

@@ -34,9 +34,10 @@ __global__ void __launch_bounds__(VNDF_STREAM_BOUND, VNDF_STREAM_MINB) stream_ke
     pdl_launch_dependents();
     pdl_wait();
     if (METHOD != kHeitz) __syncthreads();
+    const int qcap = min(a.fix_cap, kBlockFixCap);
     auto defer = [&](int64_t i) {
         const int slot = atomicAdd(&fix_count, 1);
-        if (slot < kBlockFixCap) fix_idx[slot] = i;
+        if (slot < qcap) fix_idx[slot] = i;
         else fix_one(a, PDF, i, METHOD == kCap);
     };
     const int64_t nchunks = n / V;
@@ -88,7 +89,7 @@ __global__ void __launch_bounds__(VNDF_STREAM_BOUND, VNDF_STREAM_MINB) stream_ke
     }
     if (METHOD != kHeitz) {
         __syncthreads();
-        const int m = min(fix_count, kBlockFixCap);
+        const int m = min(fix_count, qcap);
         for (int t = threadIdx.x; t < m; t += blockDim.x) fix_one(a, PDF, fix_idx[t], METHOD == kCap);
     }
 }

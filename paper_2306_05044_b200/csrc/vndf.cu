@@ -307,12 +307,26 @@ vndf_status launch_stream(const StreamArgs& a, int64_t n, cudaStream_t s) {
     }
 }
 
+// Test hook: VNDF_DEBUG_FIXUP_CAP=k (read once) shrinks every fix-up queue
+// (block queues of the streamed kernels, global queues of the fused ones) to
+// k entries, so the overflow paths (inline fix-up / full rescan) run; results
+// are bit-identical by design (tests/test_overflow_gpu.py).
+int64_t debug_fixup_cap() {
+    static const int64_t cap = [] {
+        const char* v = getenv("VNDF_DEBUG_FIXUP_CAP");
+        const long long k = v ? atoll(v) : 0;
+        return (int64_t)(k > 0 ? k : 0);
+    }();
+    return cap;
+}
+
 StreamArgs make_args(const float* wx, const float* wy, const float* wz, const float* ax,
                      const float* ay, const float* u1, const float* u2, float* hx, float* hy,
                      float* hz, float* pdf) {
     StreamArgs a;
     a.wx = wx; a.wy = wy; a.wz = wz; a.ax = ax; a.ay = ay; a.u1 = u1; a.u2 = u2;
     a.hx = hx; a.hy = hy; a.hz = hz; a.pdf = pdf;
+    a.fix_cap = debug_fixup_cap() > 0 ? (int)std::min<int64_t>(debug_fixup_cap(), kBlockFixCap) : kBlockFixCap;
     return a;
 }
 
@@ -346,6 +360,7 @@ vndf_status launch_philox_v(uint64_t seed, uint64_t first, int64_t n, float* hx,
     if (METHOD == kCap) {
         // stream-ordered transient queue: [count | cap indices]
         fq.cap = (uint64_t)std::min<int64_t>(std::max<int64_t>(n / 128, 1 << 16), (int64_t)1 << 26);
+        if (debug_fixup_cap() > 0) fq.cap = (uint64_t)debug_fixup_cap();
         e = queue_alloc(&qbuf, sizeof(unsigned long long) + fq.cap * sizeof(uint64_t), s);
         if (e != cudaSuccess) return cuda_fail(e);
         fq.count = (unsigned long long*)qbuf;
@@ -419,6 +434,7 @@ vndf_status launch_philox_reflect_v(uint64_t seed, uint64_t first, int64_t n, co
     void* qbuf = nullptr;
     if (METHOD == kCap) {
         fq.cap = (uint64_t)std::min<int64_t>(std::max<int64_t>(n / 128, 1 << 16), (int64_t)1 << 26);
+        if (debug_fixup_cap() > 0) fq.cap = (uint64_t)debug_fixup_cap();
         e = queue_alloc(&qbuf, sizeof(unsigned long long) + fq.cap * sizeof(uint64_t), s);
         if (e != cudaSuccess) return cuda_fail(e);
         fq.count = (unsigned long long*)qbuf;
