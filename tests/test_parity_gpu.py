@@ -396,9 +396,9 @@ def test_heitz_philox_conditioned_parity(env):
 
 @pytest.mark.parametrize("cfg", [(0, 0, 0), (8, 128, 1), (8, 256, 2), (4, 64, 0), (1, 128, 0), (0, 0, -1)])
 def test_launch_configurations_bit_identical(env, cfg):
-    """Persistent grid-stride grids (block-queue overflow and inline fix-ups),
-    other block sizes and vector widths give bit-identical results (the
-    tuning knob of vndf.h changes scheduling only)."""
+    """Persistent grid-stride grids (many chunks per thread and block), other
+    block sizes and vector widths give bit-identical results (the tuning knob
+    of vndf.h changes scheduling only; queue overflow: test_overflow_gpu.py)."""
     oracle, vndf, synth, dev = env
     n = (1 << 21) + 13
     x = synth.fill(5, 4, n, device=dev)
