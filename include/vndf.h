@@ -260,10 +260,15 @@ vndf_status vndf_histogram(int method, int mode, float wi_x, float wi_y, float w
 vndf_status vndf_microbench(int method, uint64_t seed, int64_t lanes, int iters, float *checksum,
                             vndf_stream_t stream);
 
-/* Tuning knobs for the streamed kernels (process-wide; 0 = automatic).
- * vector_width in {0, 1, 4, 8} caps the vector path; block_size 0 or 64..256 (multiple of 32);
- * blocks_per_sm >= 1 caps the persistent grid at SMs x blocks_per_sm, 0 uses
- * the occupancy limit, -1 launches one vector chunk per thread instead. */
+/* Tuning knobs (process-wide, all threads; 0 = each kernel family's default).
+ * Results do not depend on them (test_launch_configurations_bit_identical).
+ *   vector_width in {0, 1, 4, 8}: caps the vector path of every kernel
+ *     (1 = scalar accesses; the fused kernels honour 1 only).
+ *   block_size 0 or 64..256 (multiple of 32): threads per block of every
+ *     kernel (defaults: 128 streamed, 640 / 1024 fused cap / Heitz).
+ *   blocks_per_sm: 0 = default grid (streamed: one vector chunk per thread;
+ *     fused: one persistent block per SM); >= 1 = persistent grid-stride grid
+ *     of SMs x min(blocks_per_sm, occupancy) blocks; -1 = one chunk per thread. */
 vndf_status vndf_set_launch_config(int vector_width, int block_size, int blocks_per_sm);
 
 /* Static description of a status code. */
