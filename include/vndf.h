@@ -262,10 +262,10 @@ vndf_status vndf_microbench(int method, uint64_t seed, int64_t lanes, int iters,
 
 /* Tuning knobs (process-wide, all threads; 0 = each kernel family's default).
  * Results do not depend on them (test_launch_configurations_bit_identical).
- *   vector_width in {0, 1, 4, 8}: caps the vector path of every kernel
- *     (1 = scalar accesses; the fused kernels honour 1 only).
- *   block_size 0 or 64..256 (multiple of 32): threads per block of every
- *     kernel (defaults: 128 streamed, 640 / 1024 fused cap / Heitz).
+ *   vector_width in {0, 1, 4, 8}: caps the vector path of the sampling
+ *     kernels (1 = scalar accesses; the fused kernels honour 1 only).
+ *   block_size 0 or 64..256 (multiple of 32): threads per block of the
+ *     sampling kernels (defaults: 128 streamed, 640 / 1024 fused cap / Heitz).
  *   blocks_per_sm: 0 = default grid (streamed: one vector chunk per thread;
  *     fused: one persistent block per SM); >= 1 = persistent grid-stride grid
  *     of SMs x min(blocks_per_sm, occupancy) blocks; -1 = one chunk per thread. */
