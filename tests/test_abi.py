@@ -94,6 +94,19 @@ def test_argument_validation_without_gpu(vndf):
     assert L.vndf_count_fixups_philox(1, 0, 4, None, None) == INV
     assert L.vndf_sample_cap_pdf_host(*P, -1, None) == INV
     assert L.vndf_sample_cap_pdf_host(*P, 0, None) == vndf.VNDF_OK
+    # NEXT rows
+    assert L.vndf_sample_cap_reflect(*P, P[0], -1, None) == INV
+    assert L.vndf_sample_cap_reflect(*P[:11], None, 16, None) == INV          # weight required
+    assert L.vndf_sample_cap_reflect(*P[:7], P[0], *P[8:11], P[0], 16, None) == INV  # aliasing
+    for fn in (L.vndf_sample_cap_reflect_philox, L.vndf_sample_heitz2018_reflect_philox):
+        assert fn(1, 0, -1, *P[:5], None) == INV
+        assert fn(1, 0, 0, *P[:5], None) == vndf.VNDF_OK
+        assert fn(1, 0, 16, *P[:4], None, None) == INV                     # weight required
+        assert fn(1, 0, 16, P[0], P[0], *P[2:5], None) == INV                # outputs alias
+        assert fn(1, 0, 16, odd, *P[1:5], None) == INV                       # misaligned
+    assert L.vndf_pdf(*P[:8], None, 16, None) == INV
+    assert L.vndf_pdf(*P[:8], P[0], 16, None) == INV                         # output aliases input
+    assert L.vndf_sample_cap_pdf_native(*P, -1, None) == INV
 
 
 def test_launch_config_validation(vndf):
