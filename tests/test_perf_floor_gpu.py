@@ -1,0 +1,63 @@
+"""Loose performance floors (well below the measured values in BASELINE.md s.4)
+so that a silent slow path -- scalar accesses, a lost vector path, a fallback
+of any kind -- fails the suite instead of only the bench: the config-2 step
+>= 5.5 TB/s (measured 6.9), the fused config-4 kernel >= 150 Gsamples/s at
+2^28 (measured ~204), the end-to-end host path >= 1.0 Gsamples/s (1.72)."""
+import time
+
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_2306_05044_b200 as vndf
+    import synth
+    return vndf, synth, torch.device("cuda:0")
+
+
+def _time(fn, reps):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps  # ms
+
+
+def test_floors(env):
+    vndf, synth, dev = env
+    cfg = synth.CONFIGS[2]
+    x = synth.fill(cfg.recipe, cfg.seed, cfg.n, device=dev)
+    ins = [x[k] for k in synth.PLANES]
+    out = vndf.empty_outputs(cfg.n, dev)
+    ms = _time(lambda: vndf.vndf_sample_cap_pdf(*ins, *out), 50)
+    tbs = 44 * cfg.n / ms / 1e9
+    assert tbs >= 5.5, f"config-2 step at {tbs:.2f} TB/s"
+
+    n = 1 << 28
+    o = vndf.empty_outputs(n, dev)
+    ms = _time(lambda: vndf.vndf_sample_cap_philox(3, 0, n, *o), 5)
+    gs = n / ms / 1e6
+    assert gs >= 150, f"fused config 4 at {gs:.1f} Gsamples/s"
+    del o
+    torch.cuda.empty_cache()
+
+    hin = [t.cpu().pin_memory() for t in ins]
+    hout = [torch.empty(cfg.n, dtype=torch.float32).pin_memory() for _ in range(4)]
+    vndf.vndf_sample_cap_pdf_host(*hin, *hout)
+    t0 = time.perf_counter()
+    for _ in range(3):
+        vndf.vndf_sample_cap_pdf_host(*hin, *hout)
+    e2e = 3 * cfg.n / (time.perf_counter() - t0) / 1e9
+    assert e2e >= 1.0, f"end to end at {e2e:.2f} Gsamples/s"
