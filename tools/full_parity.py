@@ -25,7 +25,8 @@ dev = torch.device("cuda:0")
 
 
 def report(label, n, eh, ep, bad, t0):
-    print(f"{label:34s} n={n:>11d}  max|dh| {eh:.2e}  max pdf rel {ep:.2e}  "
+    pdf = f"{ep:.2e}" if ep is not None else "  (h only)"
+    print(f"{label:34s} n={n:>11d}  max|dh| {eh:.2e}  max pdf rel {pdf}  "
           f"over tolerance {bad}  ({time.time() - t0:.0f} s)", flush=True)
 
 
@@ -63,7 +64,8 @@ def streamed(cid, native=False):
             ep = max(ep, float(r.max()))
             over |= r > TOL_PDF
         bad += int(over.sum())
-    report(f"config {cid}{' native (2^24 prefix)' if native else ''}", n, eh, ep, bad, t0)
+    report(f"config {cid}{' native (2^24 prefix)' if native else ''}", n, eh,
+           ep if (cfg.pdf or native) else None, bad, t0)
     del x, out
 
 
@@ -87,8 +89,53 @@ def fused():
     report("config 4 (fused Philox)", cfg.n, eh, ep, bad, t0)
 
 
-print(f"# every sample against the float64 oracle; tolerances |dh| <= {TOL_H}, pdf rel <= {TOL_PDF}")
+TOL_WO, TOL_W = 6e-5, 1e-4  # reflection (DESIGN.md s.6.5)
+
+
+def reflect(cid):
+    cfg = synth.CONFIGS[cid]
+    t0 = time.time()
+    x = synth.fill(cfg.recipe, cfg.seed, cfg.n, device=dev)
+    out = [torch.empty(cfg.n, device=dev) for _ in range(5)]
+    vndf.vndf_sample_cap_reflect(*[x[k] for k in synth.PLANES], *out)
+    torch.cuda.synchronize()
+    _reflect_check(f"reflect, config {cid}", cfg.n, out,
+                   lambda lo, hi: oracle.batch_sample_reflect(oracle.CAP, *[x[k][lo:hi].cpu().numpy() for k in synth.PLANES]), t0)
+    del x, out
+
+
+def reflect_fused(n=1 << 28):
+    t0 = time.time()
+    out = [torch.empty(n, device=dev) for _ in range(5)]
+    vndf.vndf_sample_cap_reflect_philox(3, 0, n, *out)
+    torch.cuda.synchronize()
+    _reflect_check("reflect, fused Philox (2^28)", n, out,
+                   lambda lo, hi: oracle.batch_sample_reflect_philox(oracle.CAP, 3, np.arange(lo, hi, dtype=np.uint64)), t0)
+    del out
+
+
+def _reflect_check(label, n, out, ref_fn, t0):
+    ewo = epd = ewt = 0.0
+    bad = 0
+    for lo in range(0, n, CHUNK):
+        hi = min(n, lo + CHUNK)
+        ref = ref_fn(lo, hi)
+        got = np.stack([o[lo:hi].cpu().numpy() for o in out]).astype(np.float64)
+        a = np.abs(got[:3] - ref[:3]).max(axis=0)
+        b = np.abs(got[3] - ref[3]) / ref[3]
+        c = np.abs(got[4] - ref[4])
+        ewo, epd, ewt = max(ewo, float(a.max())), max(epd, float(b.max())), max(ewt, float(c.max()))
+        bad += int(((a > TOL_WO) | (b > TOL_PDF) | (c > TOL_W)).sum())
+    print(f"{label:34s} n={n:>11d}  max|dwo| {ewo:.2e}  max pdf rel {epd:.2e}  max|dweight| {ewt:.2e}  "
+          f"over tolerance {bad}  ({time.time() - t0:.0f} s)", flush=True)
+
+
+print(f"# every sample against the float64 oracle; tolerances |dh| <= {TOL_H}, pdf rel <= {TOL_PDF}"
+      f" (reflection: |dwo| <= {TOL_WO}, pdf rel <= {TOL_PDF}, |dweight| <= {TOL_W})")
 for cid in (1, 2, 3, 5):
     streamed(cid)
 streamed(5, native=True)
 fused()
+reflect(2)
+reflect(5)
+reflect_fused()
