@@ -110,10 +110,22 @@ class ClockSampler:
             import pynvml as nv
             nv.nvmlInit()
             self._nv = nv
-            self._h = nv.nvmlDeviceGetHandleByIndex(index)
+            self._h = self._handle(nv, index)
             self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
         except Exception:
             self._nv = None
+
+    @staticmethod
+    def _handle(nv, index):
+        """NVML handle of CUDA device `index`, matched by PCI bus id (NVML and CUDA
+        enumerate devices in different orders, and CUDA_VISIBLE_DEVICES remaps)."""
+        try:
+            import torch
+            p = torch.cuda.get_device_properties(index)
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            return nv.nvmlDeviceGetHandleByPciBusId(bus.encode())
+        except Exception:
+            return nv.nvmlDeviceGetHandleByIndex(index)
 
     def _poll(self):
         nv = self._nv
