@@ -45,7 +45,13 @@ __global__ void __launch_bounds__(128) probe(const float* const* in, float* cons
     for (int w = 0; w < W; ++w) {
         V8 o;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) o.v[j] = a[w % R].v[j] + a[(w + 1) % R].v[j] + a[(w + 3) % R].v[j];
+        for (int j = 0; j < 8; ++j) {
+            // every input plane feeds every output (so no load is dead)
+            float acc = (float)(w + 1);
+#pragma unroll
+            for (int k = 0; k < R; ++k) acc = fmaf(acc, 0.5f, a[k].v[j]);
+            o.v[j] = acc;
+        }
         st8(out[w] + c * 8, o);
     }
 }
@@ -71,6 +77,22 @@ double run(long n, const float* const* din, float* const* dout, int blocks_per_s
 }
 
 int main(int argc, char** argv) {
+    // mode "one73": a single 7-read / 3-write launch at 2^26 (for an ncu capture)
+    if (argc > 1 && std::string(argv[1]) == "one73") {
+        const long n = 1L << 26;
+        std::vector<float*> bufs(10);
+        for (auto& p : bufs) cudaMalloc(&p, n * sizeof(float));
+        const float** din;
+        float** dout;
+        cudaMallocManaged(&din, 8 * sizeof(float*));
+        cudaMallocManaged(&dout, 4 * sizeof(float*));
+        for (int k = 0; k < 7; ++k) din[k] = bufs[k];
+        for (int k = 0; k < 3; ++k) dout[k] = bufs[7 + k];
+        cudaDeviceSynchronize();
+        probe<7, 3><<<(int)((n / 8 + 127) / 128), 128>>>(din, dout, n);
+        cudaDeviceSynchronize();
+        return 0;
+    }
     // mode "stagger": planes carved from one slab with a per-plane stagger
     if (argc > 1 && std::string(argv[1]) == "stagger") {
         for (long n : {1L << 24, 1L << 26}) {

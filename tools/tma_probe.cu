@@ -103,7 +103,12 @@ __global__ void __launch_bounds__((CW + 1) * 32) tma_probe(Planes p, long n) {
         for (int w = 0; w < W; ++w) {
             float o[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) o[j] = a[w % R][j] + a[(w + 1) % R][j] + a[(w + 3) % R][j];
+            for (int j = 0; j < 8; ++j) {  // every input plane feeds every output
+                float acc = (float)(w + 1);
+#pragma unroll
+                for (int k = 0; k < R; ++k) acc = fmaf(acc, 0.5f, a[k][j]);
+                o[j] = acc;
+            }
             st8(p.out[w] + t * TILE + tid * 8, o);
         }
         if (++s == STAGES) {
