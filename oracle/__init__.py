@@ -84,6 +84,7 @@ def lib() -> ctypes.CDLL:
         L.orc_sample_raycast.argtypes = [P, d, d, u64, u64, P]
         L.orc_sample_raycast.restype = u64
         L.orc_c4_inputs.argtypes = [u64, u64, P]
+        L.orc_batch_c4_inputs.argtypes = [u64, i64, P, P]
         L.orc_batch_sample.argtypes = [i32, i64] + [P] * 7 + [P] * 5 + [i32]
         L.orc_batch_sample_philox.argtypes = [i32, u64, i64, P] + [P] * 5 + [i32]
         L.orc_batch_pdf.argtypes = [i64] + [P] * 9
@@ -91,6 +92,7 @@ def lib() -> ctypes.CDLL:
         L.orc_batch_raycast.argtypes = [P, d, d, u64, i64, P, P, P]
         L.orc_batch_raycast.restype = u64
         L.orc_batch_microbench.argtypes = [i32, u64, i64, i32, P]
+        L.orc_batch_microbench_trace.argtypes = [i32, u64, i64, i32, P]
         L.orc_G2.argtypes = [P, P, P, d, d]
         L.orc_G2.restype = d
         L.orc_brdf_cos.argtypes = [P, P, d, d]
@@ -154,6 +156,14 @@ def c4_inputs(seed: int, index: int) -> np.ndarray:
     out = np.zeros(7, dtype=np.float64)
     lib().orc_c4_inputs(seed, index, _p(out))
     return out
+
+
+def batch_c4_inputs(seed: int, indices) -> np.ndarray:
+    """Config-4 inputs (wi.xyz, ax, ay, u1, u2) at global indices, shape (7, n)."""
+    idx = np.ascontiguousarray(np.asarray(indices, dtype=np.uint64).reshape(-1))
+    out = np.empty((idx.size, 7), dtype=np.float64)
+    lib().orc_batch_c4_inputs(seed, idx.size, _p(idx), _p(out))
+    return out.T.copy()
 
 
 # --------------------------------------------------------------- scalars ---
@@ -275,6 +285,13 @@ def batch_microbench(method: int, seed: int, lanes: int, iters: int) -> np.ndarr
     """NEXT-1 microbenchmark checksums replayed in float64 (see oracle.c)."""
     out = np.empty(lanes, dtype=np.float64)
     lib().orc_batch_microbench(method, seed, lanes, iters, _p(out))
+    return out
+
+
+def batch_microbench_trace(method: int, seed: int, lanes: int, iters: int) -> np.ndarray:
+    """NEXT-1: h of every call of lanes [0, lanes), float64, shape (lanes, iters, 3)."""
+    out = np.empty((lanes, iters, 3), dtype=np.float64)
+    lib().orc_batch_microbench_trace(method, seed, lanes, iters, _p(out))
     return out
 
 

@@ -402,32 +402,39 @@ void orc_batch_sample_native(int method, int64_t n, const float *wx, const float
 }
 
 /* ------------------------------------------------------------------------ */
-/* Config-4 input recipe (DESIGN.md s.5), in float64 from the exact         */
-/* integers of ONE Philox block per sample: W = Philox(counter (i_lo, i_hi,  */
-/* 0, 0), key (seed_lo, seed_hi)) -- "key=seed, counter=sample index"       */
-/* (BASELINE.json config 4).  Bit split of the 128 bits:                    */
-/*   u1 = u(W0), u2 = u(W1)                 (24 bits each, the method's u)  */
-/*   ax = 0.01 * 100^u(W2), ay = 0.01 * 100^u(W3)   (log-uniform [0.01, 1]) */
-/*   ua = (W0[7:0] | W1[7:0] << 8) / 2^16, ub = (W2[7:0] | W3[7:0] << 8) / 2^16 */
-/*   wi uniform on the upper hemisphere: z = 1 - ua, r = sqrt(ua (2 - ua)), */
-/*      phi = 2 pi ub                                                       */
+/* Config-4 input recipe (DESIGN.md s.5 reading R12), in  */
+/* float64 from the exact integers of TWO Philox blocks per sample --       */
+/* "key=seed, counter=sample index" (BASELINE.json config 4):               */
+/*   X = Philox(counter (i_lo, i_hi, 0, 0), key (seed_lo, seed_hi))          */
+/*   Y = Philox(counter (i_lo, i_hi, 1, 0), key (seed_lo, seed_hi))          */
+/*   wi uniform on the upper hemisphere (A12 / R16):                        */
+/*      ua = u(X0), z = 1 - ua, r = sqrt(ua (2 - ua)), phi = 2 pi u(X1)     */
+/*   ax = 0.01 * 100^u(X2), ay = 0.01 * 100^u(X3)   (log-uniform [0.01, 1]) */
+/*   u1 = u(Y0), u2 = u(Y1)                  (the method's uniforms) */
+/* Every uniform carries 24 bits (u(w) = (w >> 8) 2^-24).                   */
 /* ------------------------------------------------------------------------ */
 void orc_c4_inputs(uint64_t seed, uint64_t index, double out[7])
 {
-    uint32_t W[4];
-    orc_philox_block(seed, index, 0u, W);
-    double ua = (double)((W[0] & 0xFFu) | ((W[1] & 0xFFu) << 8)) / 65536.0;
-    double ub = (double)((W[2] & 0xFFu) | ((W[3] & 0xFFu) << 8)) / 65536.0;
+    uint32_t X[4], Y[4];
+    orc_philox_block(seed, index, 0u, X);
+    orc_philox_block(seed, index, 1u, Y);
+    double ua = orc_u01(X[0]);
     double z = 1.0 - ua;
     double r = sqrt(ua * (2.0 - ua));
-    double phi = 2.0 * ORC_PI * ub;
+    double phi = 2.0 * ORC_PI * orc_u01(X[1]);
     out[0] = r * cos(phi);
     out[1] = r * sin(phi);
     out[2] = z;
-    out[3] = 0.01 * pow(100.0, orc_u01(W[2]));
-    out[4] = 0.01 * pow(100.0, orc_u01(W[3]));
-    out[5] = orc_u01(W[0]);
-    out[6] = orc_u01(W[1]);
+    out[3] = 0.01 * pow(100.0, orc_u01(X[2]));
+    out[4] = 0.01 * pow(100.0, orc_u01(X[3]));
+    out[5] = orc_u01(Y[0]);
+    out[6] = orc_u01(Y[1]);
+}
+
+/* The recipe over an index list: out7[7k .. 7k+6] (tests: distribution pins). */
+void orc_batch_c4_inputs(uint64_t seed, int64_t n, const uint64_t *indices, double *out7)
+{
+    for (int64_t k = 0; k < n; ++k) orc_c4_inputs(seed, indices[k], out7 + 7 * k);
 }
 
 /* ------------------------------------------------------------------------ */
@@ -536,21 +543,23 @@ void orc_furnace(int method, const double wa[3], double ax, double ay, uint64_t 
 /* ------------------------------------------------------------------------ */
 /* NEXT-1 sampler-only microbenchmark (the paper's GPU methodology: */
 /* Listing 1 called `iters` times per lane), replayed for lane t: inputs of  */
-/* the config-4 recipe of index t; iteration k: u1 = u(W0 + k A1), u2 =      */
-/* u(W1 + k A2) (32-bit wrap); h by the chosen listing in float64 from the   */
+/* the config-4 recipe of index t; iteration k: u1 = u(Y0 + k A1), u2 =      */
+/* u(Y1 + k A2) (32-bit wrap; Y = Philox block 1, whose words give u1, u2 of  */
+/* the recipe); h by the chosen listing in float64 from the                  */
 /* CURRENT fp32 incidence; checksum += h.x + 2 h.y + 3 h.z; then the fp32    */
 /* rotation of (wi.x, wi.y) about z with single roundings (vndf.h):          */
 /* x' = fmaf(c, x, -(s*y)), y' = fmaf(c, y, s*x).  The incidence sequence is */
 /* fp32 by definition of the benchmark; the method arithmetic is float64.    */
 /* method: 0 = cap, 1 = Heitz, 2 = cap (Listing 3 literal: same math).       */
+/* trace (nullable): receives h of every call, trace[3k .. 3k+2].           */
 /* ------------------------------------------------------------------------ */
-double orc_microbench_lane(int method, uint64_t seed, uint64_t lane, int iters)
+static double microbench_lane(int method, uint64_t seed, uint64_t lane, int iters, double *trace)
 {
     double in[7];
     orc_c4_inputs(seed, lane, in);
-    uint32_t W[4];
-    orc_philox_block(seed, lane, 0u, W);
-    uint32_t x1 = W[0], x2 = W[1];
+    uint32_t Y[4];
+    orc_philox_block(seed, lane, 1u, Y);
+    uint32_t x1 = Y[0], x2 = Y[1];
     float wx = (float)in[0], wy = (float)in[1], wz = (float)in[2];
     double ax = (double)(float)in[3], ay = (double)(float)in[4];
     const float c = 0.764842187f, s = 0.644217687f;
@@ -558,6 +567,11 @@ double orc_microbench_lane(int method, uint64_t seed, uint64_t lane, int iters)
     for (int k = 0; k < iters; ++k) {
         double wi[3] = {wx, wy, wz}, h[3];
         orc_sample_vndf(method == 1 ? 1 : 0, wi, ax, ay, orc_u01(x1), orc_u01(x2), h, NULL);
+        if (trace) {
+            trace[3 * k] = h[0];
+            trace[3 * k + 1] = h[1];
+            trace[3 * k + 2] = h[2];
+        }
         acc += h[0] + 2.0 * h[1] + 3.0 * h[2];
         x1 += 0x9E3779B9u;
         x2 += 0x7F4A7C15u;
@@ -570,9 +584,21 @@ double orc_microbench_lane(int method, uint64_t seed, uint64_t lane, int iters)
     return acc;
 }
 
+double orc_microbench_lane(int method, uint64_t seed, uint64_t lane, int iters)
+{
+    return microbench_lane(method, seed, lane, iters, NULL);
+}
+
 void orc_batch_microbench(int method, uint64_t seed, int64_t lanes, int iters, double *out)
 {
     for (int64_t t = 0; t < lanes; ++t) out[t] = orc_microbench_lane(method, seed, (uint64_t)t, iters);
+}
+
+/* Per-call h of lanes [0, lanes): trace[(t iters + k) 3 + c]. */
+void orc_batch_microbench_trace(int method, uint64_t seed, int64_t lanes, int iters, double *trace)
+{
+    for (int64_t t = 0; t < lanes; ++t)
+        microbench_lane(method, seed, (uint64_t)t, iters, trace + (size_t)t * (size_t)iters * 3u);
 }
 
 /* ------------------------------------------------------------------------ */

@@ -149,3 +149,49 @@ def test_batch_reflect_philox_driver(orc):
             x = orc.c4_inputs(9, int(i))
             want = orc.sample_reflect(method, x[:3], x[3], x[4], x[5], x[6])
             np.testing.assert_array_equal(got[:, k], want)
+
+
+# --------------------------------------------------------------- G2 pins --
+def test_G2_height_correlated_at_half_half(orc):
+    """Eq. 13-14: G2 = Gi Go / (Gi + Go - Gi Go).  With alpha = 1,
+    wm = pole and z_i = z_o = 1/3, Eq. 17 gives Gi = Go = 2z/(1+z) = 1/2, so
+    G2 = (1/4) / (3/4) = 1/3 -- the separable product Gi Go would give 1/4."""
+    z = 1.0 / 3.0
+    s = np.sqrt(1 - z * z)
+    wi = [s, 0.0, z]
+    wo = [-s * 0.6, s * 0.8, z]
+    pole = [0.0, 0.0, 1.0]
+    assert orc.G1(pole, wi, 1, 1) == pytest.approx(0.5, abs=1e-15)
+    assert orc.G1(pole, wo, 1, 1) == pytest.approx(0.5, abs=1e-15)
+    assert orc.G2(pole, wi, wo, 1, 1) == pytest.approx(1.0 / 3.0, abs=1e-14)
+
+
+def _lambda_heitz2014(w, ax, ay):
+    """Smith Lambda of the anisotropic GGX NDF (Heitz 2014, 'Understanding the
+    masking-shadowing function', eq. 86 with alpha_o^2 = ax^2 cos^2 phi +
+    ay^2 sin^2 phi): Lambda = (-1 + sqrt(1 + (ax^2 x^2 + ay^2 y^2) / z^2)) / 2."""
+    x, y, zz = w
+    a2t2 = (ax * ax * x * x + ay * ay * y * y) / (zz * zz)
+    return 0.5 * (-1.0 + np.sqrt(1.0 + a2t2))
+
+
+def test_G2_matches_heitz2014_height_correlated_form(orc):
+    """Independent textbook form of the height-correlated Smith term (Heitz 2014,
+    eq. 99): G2 = chi+(wi.wm) chi+(wo.wm) / (1 + Lambda(wi) + Lambda(wo)).
+    Random (wi, wo, alpha), wm the half vector (positive chi+ on both sides)."""
+    rng = np.random.default_rng(1314)
+    checked = 0
+    for _ in range(4000):
+        wi = rng.normal(size=3); wi[2] = abs(wi[2]) + 1e-3; wi /= np.linalg.norm(wi)
+        wo = rng.normal(size=3); wo[2] = abs(wo[2]) + 1e-3; wo /= np.linalg.norm(wo)
+        ax, ay = np.exp(rng.uniform(np.log(0.01), 0, 2))
+        wm = orc.half_vector(wi, wo)
+        want = 1.0 / (1.0 + _lambda_heitz2014(wi, ax, ay) + _lambda_heitz2014(wo, ax, ay))
+        got = orc.G2(wm, wi, wo, ax, ay)
+        assert got == pytest.approx(want, rel=1e-10, abs=1e-15)
+        # and the separable product is measurably different here
+        gi, go = orc.G1(wm, wi, ax, ay), orc.G1(wm, wo, ax, ay)
+        if want > 1e-3 and max(gi, go) < 0.9:
+            assert abs(gi * go - want) > 1e-4 * want
+        checked += 1
+    assert checked == 4000
