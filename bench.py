@@ -3,26 +3,35 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-A step is one pass of the hot path (DESIGN.md s.2: stretch, cap sample, half
-vector, unstretch, pdf, float64 fix-up of flagged samples) over one batch of
-BASELINE.json configs[1] (config 2: 2^24 samples, wi cosine-weighted, alpha
-log-uniform [0.01, 1], h + pdf), i.e. ONE launch of vndf_sample_cap_pdf.
-Inputs (28 B/sample, 470 MB) and outputs (16 B/sample) exceed the 126 MB L2,
-so no flush is needed between steps.  Under torchrun each rank processes its
-own batch (global indices rank*n ...): weak scaling, no data-path collective.
+A step is one pass of the whole hot path over one batch of BASELINE.json
+configs[3] (config 4, the largest single-GPU configuration: 2^30 samples,
+in-kernel Philox4x32-10 inputs with key = seed 3 and counter = sample index,
+wi uniform on the upper hemisphere, alpha_x, alpha_y log-uniform [0.01, 1],
+u1, u2; output h + pdf, 16 B per sample), i.e. ONE call of
+vndf_sample_cap_philox: input generation, stretch, spherical cap, half
+vector, unstretch, Eq. 1 pdf, float64 fix-up of the flagged samples (the fused
+kernel plus the fix-up kernel).  The 17.2 GB of outputs per step exceed the
+126 MB L2 many times over, so no flush is needed.  Under torchrun each rank
+processes its own batch (global indices rank * 2^30 ...): weak scaling, no
+data-path collective (DESIGN.md s.7).
 
-Prints ONE JSON line on rank 0.  `value` is whole-job Gsamples/s timed with
-CUDA events on the launching stream, max over ranks; `e2e` is the same metric
-through the blocking host-buffer entry point vndf_sample_cap_pdf_host with
-pinned host memory (copies inside the timed region); `roofline` is for the
-dominant kernel; `cpu_baseline` is the float64 oracle on this box's cores.
+Prints ONE JSON line on rank 0 (all other output goes to stderr).  `value` is
+whole-job Gsamples/s timed with CUDA events on the launching stream, max over
+ranks; `e2e` is the same metric through the blocking host-buffer entry point
+vndf_sample_cap_philox_host (pinned host outputs written across the link inside
+the timed region); `roofline` is the fused kernel's issue roofline; `c3`, `c5`,
+`c1`, `c2` are the streamed configurations (the HBM roofline run is c3);
+`cpu_baseline` is the float64 oracle on this box's cores (bounded samples), and
+its leg also checks the headline's outputs at sampled indices against it.
 `--impl reference` times the oracle itself (the tier's reference arm).
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
+import subprocess
 import sys
 import threading
 import time
@@ -33,19 +42,26 @@ if ROOT not in sys.path:
 
 METRIC = "Gsamples/s of GGX VNDF spherical-cap sampling; % HBM/FP32 roofline; vs Heitz18"
 UNIT = "Gsamples/s"
-WORKLOAD_CID = 2
-BYTES_PER_SAMPLE = {True: 44, False: 40}   # 28 B in + 16 B (h + pdf) or 12 B (h) out
+WORKLOAD_CID = 4
+C4_SEED = 3
 FALLBACK_HBM_GBS = 6650.0                   # B200_PROFILING.md fallback, if MEASURED_PEAKS.json is absent
+SMS, SMSPS_PER_SM, SM_MAX_MHZ = 148, 4, 1965.0
+TOL_H, TOL_PDF = 2e-5, 1e-4                 # BASELINE.json north_star parity contract
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
 
 
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=200)
-    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--no-variants", action="store_true", help="skip the config 3/4/5 and Heitz side runs")
+    p.add_argument("--no-variants", action="store_true", help="skip the streamed-config and NEXT side runs")
     p.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline leg")
+    p.add_argument("--no-e2e", action="store_true", help="skip the host-buffer end-to-end leg")
     return p.parse_args()
 
 
@@ -73,23 +89,26 @@ def reduce_max(value: float, world: int, device=None) -> float:
     return float(t.item())
 
 
-def peaks():
-    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+def _measured():
     try:
-        with open(path) as f:
-            mp = json.load(f)
-        return float(mp["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)", mp
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
     except Exception:
-        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)", {}
+        return {}
 
 
-def profiled_traffic(kernel_key: str):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed
-    ncu --set full summary (profiles/traffic.json), else None."""
-    path = os.path.join(ROOT, "profiles", "traffic.json")
+def peaks():
+    mp = _measured()
+    if "hbm_gbs" in mp:
+        return float(mp["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)", mp
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)", {}
+
+
+def _profiled(key: str):
+    """A per-kernel figure from the committed ncu captures (profiles/traffic.json)."""
     try:
-        with open(path) as f:
-            return json.load(f).get(kernel_key)
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(key)
     except Exception:
         return None
 
@@ -178,16 +197,13 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ timed loops ---
-def time_launches(torch, fn, steps: int, warmup: int, stream, barrier=None, per_step: bool = True):
+def time_launches(torch, fn, steps: int, warmup: int, stream, per_step: bool = True):
     """W untimed warm-up launches, then `steps` launches bracketed by events on
     `stream`.  Returns (total_ms, per_launch_ms list).  per_step=False records
-    only the two bracketing events: an event recorded between two launches
-    stops the next launch from overlapping the previous one's tail
-    (programmatic dependent launch), which a back-to-back workload does not pay."""
+    only the two bracketing events (an event between two launches stops the
+    next launch from overlapping the previous one's tail)."""
     for _ in range(warmup):
         fn()
-    if barrier:
-        barrier()
     torch.cuda.synchronize()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range((steps if per_step else 1) + 1)]
     ev[0].record(stream)
@@ -205,36 +221,45 @@ def time_launches(torch, fn, steps: int, warmup: int, stream, barrier=None, per_
     return total, [total / steps] * steps
 
 
-def cpu_baseline(host_planes, n_sample: int, budget_s: float = 12.0):
-    """The float64 oracle, as it stands, on this box's host cores, on a bounded
-    sample (the first n_sample samples of the workload, repeated until ~budget_s)."""
-    import oracle
-    import numpy as np
-    threads = oracle.default_threads()
-    planes = [np.ascontiguousarray(p[:n_sample]) for p in host_planes]
-    done, t0 = 0, time.perf_counter()
-    while True:
-        oracle.batch_sample(oracle.CAP, *planes, pdf=True, threads=threads)
-        done += n_sample
-        if time.perf_counter() - t0 >= budget_s:
-            break
-    dt = time.perf_counter() - t0
-    # one thread on a smaller slice (SURVEY 8(d): report 1 and T threads)
-    n1 = min(n_sample, 1 << 20)
-    one = [np.ascontiguousarray(p[:n1]) for p in planes]
-    done1, t1 = 0, time.perf_counter()
-    while True:
-        oracle.batch_sample(oracle.CAP, *one, pdf=True, threads=1)
-        done1 += n1
-        if time.perf_counter() - t1 >= budget_s / 6:
-            break
-    dt1 = time.perf_counter() - t1
-    return {"value": done / dt / 1e9, "unit": UNIT, "cores": threads, "kind": "oracle",
-            "sample": f"first {n_sample} samples of config 2 (float64 Listing 1+3 + Eq. 1 pdf), "
-                      f"{done // n_sample} passes in {dt:.1f} s, {threads} threads",
-            "value_1_thread": done1 / dt1 / 1e9, "cpu_model": _cpu_model()}
+# ------------------------------------------------------------- rooflines ---
+def roofline(bytes_per_launch: float, launch_ms: float, kernel_key: str):
+    """HBM roofline of a streamed kernel: algorithmic bytes / launch time against
+    the measured copy bandwidth (MEASURED_PEAKS.json)."""
+    peak, src, _ = peaks()
+    achieved = bytes_per_launch / (launch_ms * 1e-3) / 1e9
+    probe = _profiled("pattern_probe_7r4w_2e24_gbs")
+    return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": _profiled(kernel_key),
+            "peak_source": src, "kernel": kernel_key,
+            "algorithmic_bytes_per_launch": int(bytes_per_launch),
+            # context only: the HGX figure (B200_PROFILING.md) and the same plane
+            # pattern with no arithmetic (tools/bw_probe.cu)
+            "frac_of_spec_7700": round(achieved / 7700.0, 4),
+            "frac_of_pattern_probe": round(achieved / probe, 4) if probe else None}
 
 
+def issue_roofline(gsamples_s: float, key: str, n_per_launch: int = None, launch_ms: float = None):
+    """Issue roofline of a compute-bound fused kernel (DESIGN.md s.6.4): each of
+    the 4 SMSPs of the 148 SMs issues at most one warp-instruction per clock at
+    the 1965 MHz maximum SM clock (the guide's unit counts and clocks), so the
+    peak is 592 x 1.965 G warp-inst/s; achieved = the kernel's ncu-counted
+    warp-instructions per sample x samples / time.  frac is the share of issue
+    slots the kernel fills; peak / inst gives the Gsamples/s bound."""
+    inst = _profiled(key)
+    if not inst:
+        return None
+    f = SM_MAX_MHZ * 1e6
+    peak = SMS * SMSPS_PER_SM * f / 1e9
+    achieved = gsamples_s * inst
+    out = {"bound": "alu", "achieved": round(achieved, 2), "peak": round(peak, 2), "unit": "Gwarp-inst/s",
+           "frac": round(achieved / peak, 4), "traffic": None,
+           "warp_inst_per_sample": inst, "gsamples_s_bound": round(peak / inst, 2),
+           "model": f"{SMS} SMs x {SMSPS_PER_SM} SMSPs x 1 warp-inst/clk x {SM_MAX_MHZ:.0f} MHz; "
+                    f"{inst} warp-inst/sample (ncu sm__inst_executed / samples)"}
+    return out
+
+
+# ----------------------------------------------------------------- oracle ---
 def _cpu_model():
     try:
         with open("/proc/cpuinfo") as f:
@@ -246,63 +271,95 @@ def _cpu_model():
     return None
 
 
-def roofline(bytes_per_launch: float, launch_ms: float, kernel_key: str):
-    peak, src, _ = peaks()
-    achieved = bytes_per_launch / (launch_ms * 1e-3) / 1e9
-    return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "traffic": profiled_traffic(kernel_key),
-            "peak_source": src, "kernel": kernel_key,
-            "algorithmic_bytes_per_launch": int(bytes_per_launch),
-            # context only: the HGX B200 HBM3e figure (B200_PROFILING.md); the
-            # measured copy above is the denominator
-            "spec_gbs": 7700.0, "frac_of_spec": round(achieved / 7700.0, 4),
-            # context: the same 7-read / 4-write plane pattern with no arithmetic
-            # (tools/bw_probe.cu, profiles/r1/pattern_probes_r1.txt)
-            "pattern_probe_gbs": _traffic_entry("pattern_probe_7r4w_2e24_gbs")}
+def _rate(fn, n, reps, budget_s=None):
+    """Median samples/s of `reps` runs of fn() (or as many as fit in budget_s)."""
+    ts = []
+    t_end = time.perf_counter() + (budget_s or 1e9)
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        fn()
+        ts.append(time.perf_counter() - t0)
+        if budget_s and time.perf_counter() > t_end and len(ts) >= 3:
+            break
+    ts.sort()
+    return n / ts[len(ts) // 2] / 1e9, len(ts)
 
 
-def _traffic_entry(key: str):
-    """Per-pipe utilisation (fractions of peak) from the committed ncu capture
-    (profiles/traffic.json): the BASELINE metric's FP32 (fma) / SFU (xu) shares."""
+def cpu_baseline(check=None, c1_planes=None, c3_planes=None, budget_s: float = 10.0, log2_sub: int = 24):
+    """The float64 oracle, as it stands, on this box's host cores (SURVEY 8(d):
+    1 thread and T threads): the headline's config-4 recipe on bounded
+    sub-ranges, plus config 1 (median of 100, the paper's methodology)
+    and a 2^24 sub-range of config 3.  `check` = (indices, h[3, m], pdf[m]) of
+    the GPU headline run: compared with the oracle at those indices."""
+    import numpy as np
+    import oracle
+    oracle.build()
+    T = oracle.default_threads()
+    m = 1 << min(22, log2_sub)
+    idx = np.arange(m, dtype=np.uint64)
+    # headline value: config 4, 2^22 indices, T threads, repeated within the budget
+    done, t0 = 0, time.perf_counter()
+    while True:
+        oracle.batch_sample_philox(oracle.CAP, C4_SEED, idx, threads=T)
+        done += m
+        if time.perf_counter() - t0 >= budget_s * 0.4:
+            break
+    dt = time.perf_counter() - t0
+    out = {"value": round(done / dt / 1e9, 5), "unit": UNIT, "cores": T, "kind": "oracle",
+           "sample": f"config 4 recipe (float64 Philox inputs + Listing 1+3 + Eq. 1 pdf), indices [0, 2^22), "
+                     f"{done // m} passes of {m} in {dt:.1f} s on {T} threads",
+           "cpu_model": _cpu_model()}
+    sub = {}
+    ns, n1 = 1 << log2_sub, 1 << (log2_sub - 4)
+    i24 = np.arange(ns, dtype=np.uint64)
+    r1, k1 = _rate(lambda: oracle.batch_sample_philox(oracle.CAP, C4_SEED, i24[:n1], threads=1), n1, 5)
+    rT, kT = _rate(lambda: oracle.batch_sample_philox(oracle.CAP, C4_SEED, i24, threads=T), ns, 5)
+    sub["c4_2e24"] = {"T_threads": round(rT, 5), "1_thread": round(r1, 5), "runs": [kT, k1],
+                      "note": "T threads: median of 5 on [0, 2^24); 1 thread: median of 5 on [0, 2^20)"}
+    if c1_planes is not None:
+        n1p = c1_planes[0].size
+        rT, kT = _rate(lambda: oracle.batch_sample(oracle.CAP, *c1_planes, pdf=True, threads=T), n1p, 100)
+        r1, k1 = _rate(lambda: oracle.batch_sample(oracle.CAP, *c1_planes, pdf=True, threads=1), n1p, 100,
+                       budget_s=2.0)
+        sub["c1_2e16"] = {"T_threads": round(rT, 5), "1_thread": round(r1, 5), "runs": [kT, k1],
+                          "note": "median of 100 runs (1 thread: of as many as fit in 2 s)"}
+    if c3_planes is not None:
+        rT, kT = _rate(lambda: oracle.batch_sample(oracle.CAP, *c3_planes, pdf=False, threads=T),
+                       c3_planes[0].size, 5)
+        one = [p[:n1] for p in c3_planes]
+        r1, k1 = _rate(lambda: oracle.batch_sample(oracle.CAP, *one, pdf=False, threads=1), one[0].size, 5)
+        sub["c3_2e24"] = {"T_threads": round(rT, 5), "1_thread": round(r1, 5), "runs": [kT, k1],
+                          "note": "T threads: median of 5 on the first 2^24 config-3 samples; 1 thread: 2^20"}
+    out["subranges"] = sub
+    if check is not None:
+        ci, ch, cp = check
+        h_ref, p_ref, _ = oracle.batch_sample_philox(oracle.CAP, C4_SEED, ci, threads=T)
+        dh = np.abs(ch.astype(np.float64) - h_ref).max(axis=0)
+        dp = np.abs(cp.astype(np.float64) - p_ref) / p_ref
+        out["parity_vs_gpu"] = {"samples": int(ci.size), "max_abs_dh": float(dh.max()),
+                                "max_rel_dpdf": float(dp.max()), "over_tol": int(((dh > TOL_H) | (dp > TOL_PDF)).sum()),
+                                "tol": [TOL_H, TOL_PDF]}
+    return out
+
+
+# ----------------------------------------------------------------- ours ---
+def _git_sha():
     try:
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            return json.load(f).get(key)
+        return subprocess.run(["git", "-C", ROOT, "rev-parse", "HEAD"], capture_output=True, text=True,
+                              timeout=5).stdout.strip() or None
     except Exception:
         return None
 
 
-def mix_roofline(gsamples_s: float, sm_mhz: float = None):
-    """Tighter bound of the fused cap kernel (DESIGN.md s.6.4): its dynamic
-    instruction mix (ncu) weighted by dispatch cycles per instruction type
-    MEASURED on B200 (tools/pipe_probe.cu: 3-register LOP3 / IMAD.WIDE are
-    half rate), i.e. SMSP-cycles per 32 samples."""
-    cyc = _traffic_entry("cap_philox_c4_mix_cycles_per_warp_sample")
-    if not cyc:
-        return None
-    f = (sm_mhz or 1965.0) * 1e6
-    peak = 148 * 4 * f * 32 / cyc / 1e9
-    return {"achieved": round(gsamples_s, 2), "peak": round(peak, 2), "unit": "Gsamples/s",
-            "frac": round(gsamples_s / peak, 4),
-            "model": f"{cyc} dispatch cycles per 32 samples (measured per-type rates x ncu mix)"}
-
-
-def issue_roofline(gsamples_s: float, key: str, sm_mhz: float = None):
-    """Instruction-issue bound of a compute-bound kernel (DESIGN.md s.6.4): each
-    of the 4 SMSPs of the 148 SMs issues one warp-instruction per clock, so the
-    bound is 592 x f_SM / (warp-instructions per sample, ncu-counted)."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            ipc = json.load(f)[key]
-    except Exception:
-        return None
-    f = (sm_mhz or 1965.0) * 1e6
-    peak = 148 * 4 * f / ipc / 1e9
-    return {"bound": "alu", "achieved": round(gsamples_s, 2), "peak": round(peak, 2),
-            "unit": "Gsamples/s", "frac": round(gsamples_s / peak, 4),
-            "model": f"148 SMs x 4 SMSPs x 1 warp-inst/clk at {f / 1e6:.0f} MHz / {ipc} warp-inst per sample (ncu)"}
+def _sha256(tensors, limit):
+    h = hashlib.sha256()
+    for t in tensors:
+        h.update(t[:limit].cpu().numpy().tobytes())
+    return h.hexdigest()
 
 
 def run_ours(args):
+    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -316,29 +373,30 @@ def run_ours(args):
     import __graft_entry__
     __graft_entry__.build()
     import paper_2306_05044_b200 as vndf
+    from paper_2306_05044_b200 import _build
     import synth
 
     cfg = synth.CONFIGS[WORKLOAD_CID]
     n = cfg.n
+    first = shard_first_index(rank, n)
     stream = torch.cuda.current_stream(dev)
-    # weak scaling: rank r owns global samples [r n, (r + 1) n)
-    x = synth.fill(cfg.recipe, cfg.seed, n, first=shard_first_index(rank, n), device=dev)
-    ins = [x[k] for k in synth.PLANES]
+    vndf.vndf_init(dev.index)
     out = vndf.empty_outputs(n, dev, pdf=True)
     torch.cuda.synchronize()
 
     def step():
-        vndf.vndf_sample_cap_pdf(*ins, *out, n=n, stream=stream)
+        vndf.vndf_sample_cap_philox(C4_SEED, first, n, *out, stream=stream)
 
     barrier = (lambda: dist.barrier()) if world > 1 else None
-    clocks = ClockSampler(dev.index if world == 1 else local)
+    clocks = ClockSampler(dev.index)
     for _ in range(args.warmup):
         step()
+    torch.cuda.synchronize()
     if barrier:
         barrier()
     torch.cuda.synchronize()
     clocks.start()
-    total_ms, per = time_launches(torch, step, args.steps, 0, stream, per_step=False)
+    total_ms, _ = time_launches(torch, step, args.steps, 0, stream, per_step=False)
     clocks.stop()
     if barrier:
         barrier()
@@ -346,70 +404,139 @@ def run_ours(args):
     ms_per_step = total_ms / args.steps
     value = world * n * args.steps / (total_ms * 1e-3) / 1e9
 
-    # ---- end to end: host buffers through the public host entry point ----
-    e2e_steps = max(1, min(args.steps, 10))
-    hin = [p.cpu().pin_memory() for p in ins]
-    hout = [torch.empty(n, dtype=torch.float32).pin_memory() for _ in range(4)]
-    vndf.vndf_sample_cap_pdf_host(*hin, *hout, n=n)          # warm-up
-    if barrier:
-        barrier()
+    # fix-up count of the workload (diagnostic kernel, outside the timed region)
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    vndf.vndf_count_fixups_philox(C4_SEED, first, n, cnt, stream=stream)
+    # outputs at sampled indices for the oracle check (cpu_baseline leg)
+    g = torch.Generator().manual_seed(1234)
+    ci = torch.cat([torch.randint(0, n, (1 << 18,), generator=g), torch.arange(0, 4096),
+                    torch.arange(n - 4096, n)]).to(dev)
+    check_h = torch.stack([t[ci] for t in out[:3]]).cpu().numpy()
+    check_p = out[3][ci].cpu().numpy()
+    check_i = (ci.cpu().numpy().astype(np.uint64) + np.uint64(first))
+    out_sha = _sha256(out, 1 << 24)
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        vndf.vndf_sample_cap_pdf_host(*hin, *hout, n=n)
-    e2e_s = time.perf_counter() - t0
-    e2e_s = reduce_max(e2e_s, world, dev)
-    e2e = {"value": world * n * e2e_steps / e2e_s / 1e9, "unit": UNIT,
-           "h2d_bytes_per_step": 28 * n, "d2h_bytes_per_step": 16 * n,
-           "api": "vndf_sample_cap_pdf_host (pinned host buffers, blocking; zero-copy kernel over the host link)"}
+    fixups = int(cnt.item())
+    del out
+    torch.cuda.empty_cache()
+
+    rl = issue_roofline(value / world, "cap_philox_c4_warp_inst_per_sample")
+    if rl is not None:
+        rl["traffic"] = _profiled("cap_philox_c4_dram_bytes")
+        rl["algorithmic_bytes_per_launch"] = 16 * n
+        rl["pipes_ncu"] = _profiled("cap_philox_c4_pipes")
+        rl["kernel"] = "philox_kernel<cap, pdf, 8> (+ philox_fixup_kernel; timed as the whole step)"
+
+    # ---- end to end: the host-buffer entry point, pinned host outputs ----
+    e2e = None
+    if not args.no_e2e:
+        hout = [torch.empty(n, dtype=torch.float32, pin_memory=True) for _ in range(4)]
+        vndf.vndf_sample_cap_philox_host(C4_SEED, first, n, *hout)           # warm-up
+        e2e_steps = 3
+        if barrier:
+            barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            vndf.vndf_sample_cap_philox_host(C4_SEED, first, n, *hout)
+        e2e_s = reduce_max(time.perf_counter() - t0, world, dev)
+        same = bool(hashlib.sha256(b"".join(t[: 1 << 24].numpy().tobytes() for t in hout)).hexdigest() == out_sha)
+        e2e = {"value": round(world * n * e2e_steps / e2e_s / 1e9, 4), "unit": UNIT,
+               "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 16 * n,
+               "api": "vndf_sample_cap_philox_host (blocking; pinned host outputs written by the kernel "
+                      "across the host link; inputs are seed + index range, nothing host -> device)",
+               "steps": e2e_steps, "bit_identical_to_device": same,
+               "link_gb_s": round(16 * n * e2e_steps / e2e_s / 1e9, 2)}
+        del hout
 
     result = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (seeded counter-based Philox recipe, DESIGN.md s.5)",
-        "config": {"workload": f"config 2: {cfg.label}", "samples_per_gpu_per_step": n,
-                   "kernel": "vndf_sample_cap_pdf", "parallelism": f"independent shards x{world}",
-                   "l2": "inputs 470 MB + outputs 268 MB per step > 126 MB L2; no flush"},
-        "roofline": roofline(BYTES_PER_SAMPLE[True] * n, ms_per_step, "cap_pdf_c2"),
+        "data": "synthetic (in-kernel Philox4x32-10, SURVEY 8(d) config-4 recipe)",
+        "config": {"workload": f"config 4: {cfg.label}", "samples_per_gpu_per_step": n,
+                   "kernel": "vndf_sample_cap_philox", "parallelism": f"independent shards x{world}",
+                   "l2": "17.2 GB written per step >> 126 MB L2; no flush"},
+        "roofline": rl,
         "clocks": clocks.summary(),
         "e2e": e2e,
-        "gpu_launches": args.steps,
+        "gpu_launches": 2 * args.steps,
+        "fixups": {"count": fixups, "rate": round(fixups / n, 7)},
+        "build": {"git": _git_sha(), "libvndf_source_sha256": _build.source_hash()[:16]},
+        "outputs_sha256_first_2e24": out_sha[:16],
     }
 
     if world == 1 and not args.no_variants:
-        result["variants"] = variants(torch, vndf, synth, dev, stream, x, out)
+        result.update(side_runs(torch, vndf, synth, dev, stream, value))
     if rank == 0 and world == 1 and not args.no_cpu:
-        host = [p.cpu().numpy() for p in ins]
-        result["cpu_baseline"] = cpu_baseline(host, 1 << 22)
+        c1 = synth.CONFIGS[1]
+        c1p = [v.cpu().numpy() for v in synth.fill(c1.recipe, c1.seed, c1.n, device=dev).values()]
+        c3 = synth.CONFIGS[3]
+        x3 = synth.fill(c3.recipe, c3.seed, 1 << 24, device=dev)
+        c3p = [x3[k].cpu().numpy() for k in synth.PLANES]
+        del x3
+        cb = cpu_baseline(check=(check_i, check_h, check_p), c1_planes=c1p, c3_planes=c3p)
+        result["parity"] = cb.pop("parity_vs_gpu")
+        result["cpu_baseline"] = cb
     elif rank == 0:
         result["cpu_baseline"] = None
     if rank == 0:
-        print(json.dumps(result), flush=True)
+        print(json.dumps(result, separators=(",", ":")), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
-def variants(torch, vndf, synth, dev, stream, x2, out2):
-    """Side measurements on identical inputs (not the headline): Heitz-2018 on
-    config 2, configs 3/4/5 (cap and Heitz), each 3 warm-up + 20 timed launches."""
+def side_runs(torch, vndf, synth, dev, stream, c4_value):
+    """The other configurations and the Heitz-2018 baseline on identical inputs
+    (3 warm-up + 20 timed launches each), compact: c4 Heitz ratio, c3 (HBM
+    roofline run), c5 (edge mix), c1 (latency), c2, then the NEXT rows."""
     res = {}
     reps, warm = 20, 3
 
-    def timed(fn):
-        total, per = time_launches(torch, fn, reps, warm, stream, per_step=False)
-        return total / reps
+    def timed(fn, r=reps):
+        total, _ = time_launches(torch, fn, r, warm, stream, per_step=False)
+        return total / r
 
-    n2 = x2["wi_x"].numel()
-    ins2 = [x2[k] for k in synth.PLANES]
-    t_cap = timed(lambda: vndf.vndf_sample_cap_pdf(*ins2, *out2, stream=stream))
-    t_hz = timed(lambda: vndf.vndf_sample_heitz2018(*ins2, *out2, stream=stream))
-    res["c2_cap_pdf"] = {"gsamples_s": n2 / t_cap / 1e6, "ms": t_cap}
-    res["c2_heitz_pdf"] = {"gsamples_s": n2 / t_hz / 1e6, "ms": t_hz, "t_heitz_over_t_cap": t_hz / t_cap}
+    def gs(n, ms):
+        return round(n / ms / 1e6, 2)
 
-    # config 1: 2^16 samples, L2-resident and launch-bound (SURVEY 8(d): report
-    # us per launch): 50 launches captured in one CUDA graph, replayed, so the
-    # device time per launch is measured without the host's per-call cost
+    c4 = synth.CONFIGS[4]
+    o4 = vndf.empty_outputs(c4.n, dev)
+    t_h4 = timed(lambda: vndf.vndf_sample_heitz2018_philox(C4_SEED, 0, c4.n, *o4, stream=stream), 10)
+    hz = gs(c4.n, t_h4)
+    res["heitz_c4"] = {"gsamples_s": hz, "t_heitz_over_t_cap": round(c4_value / hz, 4),
+                       "roofline": issue_roofline(hz, "heitz_philox_c4_warp_inst_per_sample")}
+    del o4
+    torch.cuda.empty_cache()
+
+    # config 3: 2^28 streamed, h only -- the HBM roofline run
+    c3 = synth.CONFIGS[3]
+    x3 = synth.fill(c3.recipe, c3.seed, c3.n, device=dev)
+    o3 = vndf.empty_outputs(c3.n, dev, pdf=False)
+    ins3 = [x3[k] for k in synth.PLANES]
+    t_cap3 = timed(lambda: vndf.vndf_sample_cap(*ins3, *o3, stream=stream))
+    t_hz3 = timed(lambda: vndf.vndf_sample_heitz2018(*ins3, *o3, None, stream=stream))
+    rl3 = roofline(40 * c3.n, t_cap3, "cap_c3")
+    res["c3"] = {"gsamples_s": gs(c3.n, t_cap3), "ms": round(t_cap3, 4), "gb_s": rl3["achieved"],
+                 "frac_hbm": rl3["frac"], "t_heitz_over_t_cap": round(t_hz3 / t_cap3, 4), "roofline": rl3}
+    del x3, o3, ins3
+    torch.cuda.empty_cache()
+
+    # config 5: 2^26 edge mix, h + pdf (flip frame and the native frame)
+    c5 = synth.CONFIGS[5]
+    x5 = synth.fill(c5.recipe, c5.seed, c5.n, device=dev)
+    o5 = vndf.empty_outputs(c5.n, dev)
+    ins5 = [x5[k] for k in synth.PLANES]
+    t_cap5 = timed(lambda: vndf.vndf_sample_cap_pdf(*ins5, *o5, stream=stream))
+    t_hz5 = timed(lambda: vndf.vndf_sample_heitz2018(*ins5, *o5, stream=stream))
+    t_nat5 = timed(lambda: vndf.vndf_sample_cap_pdf_native(*ins5, *o5, stream=stream))
+    res["c5"] = {"gsamples_s": gs(c5.n, t_cap5), "t_heitz_over_t_cap": round(t_hz5 / t_cap5, 4),
+                 "frac_hbm": roofline(44 * c5.n, t_cap5, "cap_pdf_c5")["frac"],
+                 "native_gsamples_s": gs(c5.n, t_nat5)}
+    del x5, o5, ins5
+
+    # config 1: 2^16 samples, L2-resident and launch-bound (SURVEY 8(d): us per
+    # launch): 50 launches in one CUDA graph, replayed
     c1 = synth.CONFIGS[1]
     x1 = synth.fill(c1.recipe, c1.seed, c1.n, device=dev)
     o1 = vndf.empty_outputs(c1.n, dev)
@@ -418,7 +545,7 @@ def variants(torch, vndf, synth, dev, stream, x2, out2):
     vndf.vndf_sample_heitz2018(*ins1, *o1)
     torch.cuda.synchronize()
     c1res = {}
-    for name, fn in (("cap", vndf.vndf_sample_cap_pdf), ("heitz", vndf.vndf_sample_heitz2018)):
+    for name, fn in (("cap_us", vndf.vndf_sample_cap_pdf), ("heitz_us", vndf.vndf_sample_heitz2018)):
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             for _ in range(50):
@@ -431,106 +558,22 @@ def variants(torch, vndf, synth, dev, stream, x2, out2):
             g.replay()
         ev1.record()
         torch.cuda.synchronize()
-        us = ev0.elapsed_time(ev1) * 1e3 / 500
-        c1res[name] = {"us_per_launch": us, "gsamples_s": c1.n / us / 1e3}
-    c1res["t_heitz_over_t_cap"] = c1res["heitz"]["us_per_launch"] / c1res["cap"]["us_per_launch"]
-    res["c1_latency"] = c1res
+        c1res[name] = round(ev0.elapsed_time(ev1) * 1e3 / 500, 3)
+    c1res["t_heitz_over_t_cap"] = round(c1res["heitz_us"] / c1res["cap_us"], 4)
+    res["c1"] = c1res
     del x1, o1, ins1
 
-    # config 3: 2^28 streamed, h only
-    c3 = synth.CONFIGS[3]
-    x3 = synth.fill(c3.recipe, c3.seed, c3.n, device=dev)
-    o3 = vndf.empty_outputs(c3.n, dev, pdf=False)
-    ins3 = [x3[k] for k in synth.PLANES]
-    t_cap3 = timed(lambda: vndf.vndf_sample_cap(*ins3, *o3, stream=stream))
-    t_hz3 = timed(lambda: vndf.vndf_sample_heitz2018(*ins3, *o3, None, stream=stream))
-    rl = roofline(BYTES_PER_SAMPLE[False] * c3.n, t_cap3, "cap_c3")
-    res["c3_cap"] = {"gsamples_s": c3.n / t_cap3 / 1e6, "ms": t_cap3, "gb_s": rl["achieved"],
-                     "frac_hbm": rl["frac"]}
-    res["c3_heitz"] = {"gsamples_s": c3.n / t_hz3 / 1e6, "ms": t_hz3, "t_heitz_over_t_cap": t_hz3 / t_cap3}
-    del x3, o3, ins3
+    # config 2: 2^24, h + pdf
+    c2 = synth.CONFIGS[2]
+    x2 = synth.fill(c2.recipe, c2.seed, c2.n, device=dev)
+    o2 = vndf.empty_outputs(c2.n, dev)
+    ins2 = [x2[k] for k in synth.PLANES]
+    t_cap2 = timed(lambda: vndf.vndf_sample_cap_pdf(*ins2, *o2, stream=stream))
+    t_hz2 = timed(lambda: vndf.vndf_sample_heitz2018(*ins2, *o2, stream=stream))
+    res["c2"] = {"gsamples_s": gs(c2.n, t_cap2), "frac_hbm": roofline(44 * c2.n, t_cap2, "cap_pdf_c2")["frac"],
+                 "t_heitz_over_t_cap": round(t_hz2 / t_cap2, 4)}
 
-    # config 5: 2^26 edge mix, h + pdf
-    c5 = synth.CONFIGS[5]
-    x5 = synth.fill(c5.recipe, c5.seed, c5.n, device=dev)
-    o5 = vndf.empty_outputs(c5.n, dev)
-    ins5 = [x5[k] for k in synth.PLANES]
-    t_cap5 = timed(lambda: vndf.vndf_sample_cap_pdf(*ins5, *o5, stream=stream))
-    t_hz5 = timed(lambda: vndf.vndf_sample_heitz2018(*ins5, *o5, stream=stream))
-    t_nat5 = timed(lambda: vndf.vndf_sample_cap_pdf_native(*ins5, *o5, stream=stream))
-    res["c5_cap_pdf_native"] = {"gsamples_s": c5.n / t_nat5 / 1e6, "ms": t_nat5}
-    res["c5_cap_pdf"] = {"gsamples_s": c5.n / t_cap5 / 1e6, "ms": t_cap5}
-    res["c5_heitz_pdf"] = {"gsamples_s": c5.n / t_hz5 / 1e6, "ms": t_hz5, "t_heitz_over_t_cap": t_hz5 / t_cap5}
-    del x5, o5, ins5
-
-    # config 4: 2^30 fused Philox, h + pdf (17 GB written per launch)
-    c4 = synth.CONFIGS[4]
-    o4 = vndf.empty_outputs(c4.n, dev)
-    t_cap4 = timed(lambda: vndf.vndf_sample_cap_philox(c4.seed, 0, c4.n, *o4, stream=stream))
-    t_hz4 = timed(lambda: vndf.vndf_sample_heitz2018_philox(c4.seed, 0, c4.n, *o4, stream=stream))
-    res["c4_cap_philox"] = {"gsamples_s": c4.n / t_cap4 / 1e6, "ms": t_cap4,
-                            "write_gb_s": 16 * c4.n / t_cap4 / 1e6,
-                            "roofline": issue_roofline(c4.n / t_cap4 / 1e6, "cap_philox_c4_warp_inst_per_sample"),
-                            "mix_bound": mix_roofline(c4.n / t_cap4 / 1e6),
-                            "pipes_ncu": _traffic_entry("cap_philox_c4_pipes")}
-    res["c4_heitz_philox"] = {"gsamples_s": c4.n / t_hz4 / 1e6, "ms": t_hz4,
-                              "t_heitz_over_t_cap": t_hz4 / t_cap4,
-                              "roofline": issue_roofline(c4.n / t_hz4 / 1e6, "heitz_philox_c4_warp_inst_per_sample"),
-                              "pipes_ncu": _traffic_entry("heitz_philox_c4_pipes")}
-    del o4
-    torch.cuda.empty_cache()
-
-    # NEXT-2: reflection sampling on the config-2 inputs (28 B in, 20 B out)
-    ro = [torch.empty(n2, dtype=torch.float32, device=dev) for _ in range(5)]
-    t_r = timed(lambda: vndf.vndf_sample_cap_reflect(*ins2, *ro, stream=stream))
-    rl = roofline(48 * n2, t_r, "cap_reflect_c2")
-    res["c2_cap_reflect"] = {"gsamples_s": n2 / t_r / 1e6, "ms": t_r, "gb_s": rl["achieved"], "frac_hbm": rl["frac"]}
-    # NEXT-4: Eq. 1 at caller-provided h (the h just sampled), 32 B in + 4 B out
-    t_p = timed(lambda: vndf.vndf_pdf(*ro[:3], *ins2[:5], ro[3], stream=stream))
-    rl = roofline(36 * n2, t_p, "pdf_c2")
-    res["c2_pdf"] = {"gsamples_s": n2 / t_p / 1e6, "ms": t_p, "gb_s": rl["achieved"], "frac_hbm": rl["frac"]}
-    # NEXT-3: native below-horizon handling on the config-5 inputs is measured below
-    del ro
-    # NEXT-2: Eq. 19 white-furnace estimator (compute-bound), cap vs Heitz, 2^28 samples
-    sums = torch.zeros(2, dtype=torch.float64, device=dev)
-    nf = 1 << 28
-    wa = (0.5, 0.2, 0.8426149773176359)
-    fur = {}
-    for method, name in ((0, "cap"), (1, "heitz")):
-        t = timed(lambda: vndf.vndf_furnace(method, wa, (0.3, 0.1), 17, nf, sums, stream=stream))
-        torch.cuda.synchronize()
-        s1, s2 = sums.cpu().tolist()
-        fur[name] = {"gsamples_s": nf / t / 1e6, "ms": t, "estimate": s1 / nf,
-                     "variance": s2 / nf - (s1 / nf) ** 2}
-    fur["t_heitz_over_t_cap"] = fur["heitz"]["ms"] / fur["cap"]["ms"]
-    res["furnace_eq19"] = fur
-
-    # NEXT-2 fused: config-4 inputs in-kernel, reflection + Eq. 20 pdf + weight
-    nr = 1 << 28
-    orf = [torch.empty(nr, dtype=torch.float32, device=dev) for _ in range(5)]
-    t_rc = timed(lambda: vndf.vndf_sample_cap_reflect_philox(3, 0, nr, *orf, stream=stream))
-    t_rh = timed(lambda: vndf.vndf_sample_heitz2018_reflect_philox(3, 0, nr, *orf, stream=stream))
-    res["reflect_philox"] = {
-        "cap": {"gsamples_s": nr / t_rc / 1e6, "ms": t_rc, "write_gb_s": 20 * nr / t_rc / 1e6,
-                "roofline": issue_roofline(nr / t_rc / 1e6, "cap_reflect_philox_warp_inst_per_sample")},
-        "heitz": {"gsamples_s": nr / t_rh / 1e6, "ms": t_rh,
-                  "roofline": issue_roofline(nr / t_rh / 1e6, "heitz_reflect_philox_warp_inst_per_sample")},
-        "t_heitz_over_t_cap": t_rh / t_rc}
-    del orf
-
-    # NEXT-3: device histograms (2^28 samples of one (wi, alpha) into 64 x 64
-    # shared-memory bins; the chi-square tests' workhorse)
-    cnt = torch.zeros(64 * 64, dtype=torch.int64, device=dev)
-    hist = {}
-    for method, name in ((0, "cap"), (1, "heitz"), (2, "cap_native")):
-        wi_h = (0.5, 0.2, 0.8426149773176359) if method != 2 else (0.5, 0.2, -0.8426149773176359)
-        t_h = timed(lambda: vndf.vndf_histogram(method, 0, wi_h, (0.3, 0.1), 17, 1 << 28, 64, 64, cnt,
-                                                stream=stream))
-        hist[name] = {"gsamples_s": (1 << 28) / t_h / 1e6, "ms": t_h}
-    hist["note"] = ("audit kernel: time dominated by binning (acos, atan2, shared atomics); the cap "
-                    "path's float64 fix-ups run inline here, so this is no sampler comparison")
-    res["histogram_next3"] = hist
-
+    nxt = {}
     # NEXT-1: sampler-only microbenchmark in the paper's methodology:
     # 64 Listing-1 calls per lane, median of 100 dispatches
     lanes, iters = 148 * 2048 * 16, 64
@@ -539,25 +582,52 @@ def variants(torch, vndf, synth, dev, stream, x2, out2):
     for method, name in ((0, "cap"), (1, "heitz"), (2, "cap_literal")):
         _, per = time_launches(torch, lambda: vndf.vndf_microbench(method, 5, lanes, iters, ck, stream=stream),
                                100, 5, stream)
-        med = sorted(per)[len(per) // 2]
-        gs = lanes * iters / med / 1e6
-        mb[name] = {"gsamples_s": gs, "median_ms": med,
-                    "roofline": issue_roofline(gs, f"microbench_{name}_warp_inst_per_sample")}
-    mb["t_heitz_over_t_cap"] = mb["heitz"]["median_ms"] / mb["cap"]["median_ms"]
-    mb["t_heitz_over_t_cap_literal"] = mb["heitz"]["median_ms"] / mb["cap_literal"]["median_ms"]
-    mb["paper"] = "t_Heitz/t_cap 1.3925 on RTX 2080, 1.5296 on Arc A770 (P:814-821)"
-    res["microbench_64_per_lane"] = mb
+        mb[name] = sorted(per)[len(per) // 2]
+    nxt["microbench_t_heitz_over_t_cap"] = round(mb["heitz"] / mb["cap"], 4)
+    nxt["microbench_t_heitz_over_t_cap_literal"] = round(mb["heitz"] / mb["cap_literal"], 4)
+    nxt["microbench_cap_gsamples_s"] = gs(lanes * iters, mb["cap"])
     del ck
-    def rnd(v):
-        if isinstance(v, dict):
-            return {k: rnd(x) for k, x in v.items()}
-        return round(v, 4) if isinstance(v, float) else v
-    return rnd(res)
+    # NEXT-2: reflection on the config-2 inputs; fused on config-4 inputs
+    ro = [torch.empty(c2.n, dtype=torch.float32, device=dev) for _ in range(5)]
+    t_r = timed(lambda: vndf.vndf_sample_cap_reflect(*ins2, *ro, stream=stream))
+    nxt["reflect_c2_frac_hbm"] = roofline(48 * c2.n, t_r, "cap_reflect_c2")["frac"]
+    # NEXT-4: Eq. 1 at caller-provided h
+    t_p = timed(lambda: vndf.vndf_pdf(*ro[:3], *ins2[:5], ro[3], stream=stream))
+    nxt["pdf_c2_frac_hbm"] = roofline(36 * c2.n, t_p, "pdf_c2")["frac"]
+    del ro, x2, o2, ins2
+    nr = 1 << 28
+    orf = [torch.empty(nr, dtype=torch.float32, device=dev) for _ in range(5)]
+    t_rc = timed(lambda: vndf.vndf_sample_cap_reflect_philox(C4_SEED, 0, nr, *orf, stream=stream))
+    t_rh = timed(lambda: vndf.vndf_sample_heitz2018_reflect_philox(C4_SEED, 0, nr, *orf, stream=stream))
+    nxt["reflect_philox_gsamples_s"] = gs(nr, t_rc)
+    nxt["reflect_philox_t_heitz_over_t_cap"] = round(t_rh / t_rc, 4)
+    del orf
+    # NEXT-2: Eq. 19 white-furnace estimator (same variance reduction)
+    sums = torch.zeros(2, dtype=torch.float64, device=dev)
+    nf = 1 << 28
+    wa = (0.5, 0.2, 0.8426149773176359)
+    fur = {}
+    for method, name in ((0, "cap"), (1, "heitz")):
+        t = timed(lambda: vndf.vndf_furnace(method, wa, (0.3, 0.1), 17, nf, sums, stream=stream))
+        torch.cuda.synchronize()
+        s1, s2 = sums.cpu().tolist()
+        fur[name] = (t, s1 / nf, s2 / nf - (s1 / nf) ** 2)
+    nxt["furnace_t_heitz_over_t_cap"] = round(fur["heitz"][0] / fur["cap"][0], 4)
+    nxt["furnace_estimate_var"] = [round(fur["cap"][1], 5), round(fur["cap"][2], 5),
+                                   round(fur["heitz"][1], 5), round(fur["heitz"][2], 5)]
+    # NEXT-3: device histogram throughput (2^28 samples into 64 x 64 bins)
+    cnt = torch.zeros(64 * 64, dtype=torch.int64, device=dev)
+    t_h = timed(lambda: vndf.vndf_histogram(0, 0, wa, (0.3, 0.1), 17, 1 << 28, 64, 64, cnt, stream=stream), 5)
+    nxt["histogram_gsamples_s"] = gs(1 << 28, t_h)
+    torch.cuda.empty_cache()
+    res["next"] = nxt
+    return res
 
 
 def run_reference(args):
     """The tier's reference arm: the float64 oracle, as it stands, on this box's
-    host cores; each step a bounded 2^22-sample slice of the config-2 workload."""
+    host cores; each step a bounded 2^22-sample slice (indices [0, 2^22)) of the
+    config-4 workload.  Under torchrun only rank 0 runs."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
@@ -567,14 +637,13 @@ def run_reference(args):
     oracle.build()
     cfg = synth.CONFIGS[WORKLOAD_CID]
     m = 1 << 22
-    x = synth.fill_numpy(cfg.recipe, cfg.seed, m)
-    planes = [x[k] for k in synth.PLANES]
+    idx = np.arange(m, dtype=np.uint64)
     threads = oracle.default_threads()
     for _ in range(args.warmup):
-        oracle.batch_sample(oracle.CAP, *planes, pdf=True, threads=threads)
+        oracle.batch_sample_philox(oracle.CAP, C4_SEED, idx, threads=threads)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        oracle.batch_sample(oracle.CAP, *planes, pdf=True, threads=threads)
+        oracle.batch_sample_philox(oracle.CAP, C4_SEED, idx, threads=threads)
     dt = time.perf_counter() - t0
     value = m * args.steps / dt / 1e9
     print(json.dumps({
@@ -582,13 +651,12 @@ def run_reference(args):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (same recipe as ours)",
-        "config": {"workload": f"config 2: {cfg.label}", "samples_per_step": m,
-                   "note": "each step a bounded 2^22-sample slice of the 2^24-sample workload"},
+        "config": {"workload": f"config 4: {cfg.label}", "samples_per_step": m,
+                   "note": "each step a bounded 2^22-sample slice of the 2^30-sample workload"},
         "cpu_baseline": {"value": round(value, 5), "unit": UNIT, "cores": threads, "kind": "oracle",
-                         "sample": f"2^22 config-2 samples per step, {threads} threads"},
+                         "sample": f"config-4 indices [0, 2^22) per step, {threads} threads"},
         "e2e": {"value": round(value, 5), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
-    _ = np
 
 
 def main():

@@ -41,15 +41,18 @@
  *   - Calls only ENQUEUE work on `stream` (NULL = legacy default stream) and
  *     return; outputs are valid once the caller synchronises the stream.
  *     The *_host call is the exception: it is blocking.
- *   - The device calls can be captured into a CUDA graph (stream capture) once
- *     the device's global state exists, i.e. after one call of the same kind
- *     on that device outside capture (the first fused call uploads the sine
- *     table synchronously).  Replays recompute from the captured buffers.
+ *   - The device calls never synchronise and never copy host data, so every
+ *     device call, including the first one in the process, can be captured
+ *     into a CUDA graph (stream capture).  (The very first libvndf call of a
+ *     process starts the CUDA runtime inside the library, which waits for
+ *     work already queued on the device; vndf_init does that up front.)  Replays recompute from the captured
+ *     buffers.  The device a call runs on is the device of `stream` (the
+ *     current device for the NULL stream); all its buffers must live there.
  *   - Thread-safe.  Global state, per device, created on first use and kept
  *     for the life of the process: cached device attributes and launch
- *     configurations, a 64 KB sine table (fused Philox path), a private
- *     stream-ordered memory pool for transient fix-up queues, and the host
- *     entry point's staging area (see vndf_release_host_staging).
+ *     configurations, a private stream-ordered memory pool for transient
+ *     fix-up queues (released with vndf_release_host_staging), and the host
+ *     entry points' staging area (see vndf_release_host_staging).
  *   - Outputs are a pure function of the inputs (of seed and global index for
  *     the Philox calls): independent of grid, stream, vector path or chunking.
  *
@@ -118,14 +121,14 @@ vndf_status vndf_sample_heitz2018(const float *wi_x, const float *wi_y, const fl
                                   int64_t n, vndf_stream_t stream);
 
 /* Fused in-kernel Philox4x32-10 (BASELINE config 4: key = seed, counter =
- * sample index).  Sample k of the call has global index i = first_index + k
- * and ONE Philox block W = Philox(counter (i_lo, i_hi, 0, 0), key (seed_lo,
- * seed_hi)); u(w) = (w >> 8) 2^-24.  Its 128 bits give
- *   u1 = u(W0), u2 = u(W1);
- *   alpha_x = 0.01 * 100^u(W2), alpha_y = 0.01 * 100^u(W3);
- *   wi uniform on the upper hemisphere from 16-bit uniforms
- *      ua = (W0[7:0] | W1[7:0] << 8) 2^-16, ub = (W2[7:0] | W3[7:0] << 8) 2^-16:
- *      z = 1 - ua, r = sqrt(ua (2 - ua)), phi = 2 pi ub.
+ * sample index).  Sample k of the call has global index
+ * i = first_index + k and TWO Philox blocks, key (seed_lo, seed_hi):
+ *   X = Philox(counter (i_lo, i_hi, 0, 0)),  Y = Philox(counter (i_lo, i_hi, 1, 0));
+ * with u(w) = (w >> 8) 2^-24 (24 bits):
+ *   wi uniform on the upper hemisphere: z = 1 - u(X0), r = sqrt(u(X0) (2 - u(X0))),
+ *      phi = 2 pi u(X1), wi = (r cos phi, r sin phi, z);
+ *   alpha_x = 0.01 * 100^u(X2), alpha_y = 0.01 * 100^u(X3);
+ *   u1 = u(Y0), u2 = u(Y1).
  * Outputs h and pdf (16 B per sample); pdf may be NULL. */
 vndf_status vndf_sample_cap_philox(uint64_t seed, uint64_t first_index, int64_t n,
                                    float *h_x, float *h_y, float *h_z, float *pdf,
@@ -148,8 +151,9 @@ vndf_status vndf_philox4x32_10(uint64_t seed, uint64_t first_index, int64_t n,
  *   default under unified addressing), the kernel reads the inputs and writes
  *   the outputs across the host link in place (zero-copy), on `stream`.
  * - Otherwise (pageable memory) the batch is streamed through the GPU in
- *   chunks of 2 Mi samples, overlapping host->device copies, the kernel and
- *   device->host copies on three library-owned streams.  Device staging
+ *   chunks of 2 Mi samples on three library-owned streams (copies from and
+ *   to pageable memory are staged by the driver and complete synchronously,
+ *   so chunks overlap little: pin the buffers for throughput).  Device staging
  *   (3 x 2 Mi x 44 B = 277 MB per device) is allocated on first use and kept
  *   for later calls; vndf_release_host_staging() frees it.
  * BLOCKING: returns when the outputs are in host memory.  Work is ordered
@@ -161,8 +165,24 @@ vndf_status vndf_sample_cap_pdf_host(const float *wi_x, const float *wi_y, const
                                      float *h_x, float *h_y, float *h_z, float *pdf,
                                      int64_t n, vndf_stream_t stream);
 
-/* Frees the cached staging of vndf_sample_cap_pdf_host on every device.
- * VNDF_ERR_INVALID_ARGUMENT if a host call is in flight on another thread. */
+/* End-to-end form of vndf_sample_cap_philox (BASELINE config 4) writing HOST
+ * buffers h_x, h_y, h_z, pdf (pdf may be NULL); the inputs are generated in
+ * the kernel, so nothing crosses the link host -> device.
+ * - Page-locked, device-mapped outputs (cudaHostAlloc / torch pin_memory()):
+ *   the kernel writes them across the host link in place (zero-copy).
+ * - Otherwise (pageable memory) chunks of 2 Mi samples are computed into the
+ *   device staging of vndf_sample_cap_pdf_host and copied device -> host;
+ *   pageable copies complete synchronously, so this path does not overlap.
+ * BLOCKING; ordered after prior work on `stream`; results bit-identical to
+ * vndf_sample_cap_philox with the same seed and first_index. */
+vndf_status vndf_sample_cap_philox_host(uint64_t seed, uint64_t first_index, int64_t n,
+                                        float *h_x, float *h_y, float *h_z, float *pdf,
+                                        vndf_stream_t stream);
+
+/* Frees the cached staging of the host entry points on every device and
+ * trims the library's fix-up-queue memory pools to zero (it waits for the
+ * devices to go idle first).  VNDF_ERR_INVALID_ARGUMENT if a host call is in
+ * flight on another thread. */
 vndf_status vndf_release_host_staging(void);
 
 /* Diagnostic: number of samples the spherical-cap kernels would route to the
@@ -248,8 +268,8 @@ vndf_status vndf_histogram(int method, int mode, float wi_x, float wi_y, float w
 /* Sampler-only microbenchmark in the paper's GPU methodology (P:814-817:
  * "calls Listing 1 64 times per lane").  Lane t (0 <= t < lanes) draws wi and
  * (alpha_x, alpha_y) once from the config-4 recipe of index t (seed), then for
- * k = 0 .. iters-1 samples h with u1 = u(W0 + k 0x9E3779B9), u2 = u(W1 + k
- * 0x7F4A7C15) (32-bit wrap-around; W = that lane's Philox block), adds
+ * k = 0 .. iters-1 samples h with u1 = u(Y0 + k 0x9E3779B9), u2 = u(Y1 + k
+ * 0x7F4A7C15) (32-bit wrap-around; Y = that lane's Philox block 1), adds
  * h.x + 2 h.y + 3 h.z to an fp32 checksum, and rotates wi about z:
  * (x, y) <- (fma(c, x, -(s y)), fma(c, y, s x)) with c = 0.764842187f,
  * s = 0.644217687f, every operation rounded to fp32 (so no call is
@@ -260,16 +280,33 @@ vndf_status vndf_histogram(int method, int mode, float wi_x, float wi_y, float w
 vndf_status vndf_microbench(int method, uint64_t seed, int64_t lanes, int iters, float *checksum,
                             vndf_stream_t stream);
 
+/* vndf_microbench that also records every call (tests, element-wise parity of
+ * NEXT-1): trace[4 (t iters + k) + c] = (h.x, h.y, h.z, flag) of call k of
+ * lane t, flag = 1.0f when the spherical-cap conditioning test marks the call
+ * (the production kernels would recompute it in float64; always 0 for methods
+ * 1 and 2).  trace: device pointer to 4 lanes iters floats, 16-byte aligned;
+ * checksum as for vndf_microbench (must not overlap trace). */
+vndf_status vndf_microbench_trace(int method, uint64_t seed, int64_t lanes, int iters, float *checksum,
+                                  float *trace, vndf_stream_t stream);
+
 /* Tuning knobs (process-wide, all threads; 0 = each kernel family's default).
  * Results do not depend on them (test_launch_configurations_bit_identical).
  *   vector_width in {0, 1, 4, 8}: caps the vector path of the sampling
  *     kernels (1 = scalar accesses; the fused kernels honour 1 only).
  *   block_size 0 or 64..256 (multiple of 32): threads per block of the
- *     sampling kernels (defaults: 128 streamed, 640 / 1024 fused cap / Heitz).
+ *     sampling kernels (defaults: 128 streamed, 256 fused).
  *   blocks_per_sm: 0 = default grid (streamed: one vector chunk per thread;
- *     fused: one persistent block per SM); >= 1 = persistent grid-stride grid
+ *     fused: persistent, SMs x resident blocks); >= 1 = persistent grid-stride grid
  *     of SMs x min(blocks_per_sm, occupancy) blocks; -1 = one chunk per thread. */
 vndf_status vndf_set_launch_config(int vector_width, int block_size, int blocks_per_sm);
+
+/* Initialises the library's CUDA state on `device` (-1 = the current device)
+ * and waits for it: the CUDA runtime's one-time start-up in this process
+ * (loading libvndf's kernels into the context waits for the work already
+ * queued on the device: tools/first_call_probe.py), the cached device
+ * attributes and the fix-up queue pool.  Optional: the first call of any
+ * entry point does the same implicitly.  After it, calls only enqueue. */
+vndf_status vndf_init(int device);
 
 /* Static description of a status code. */
 const char *vndf_status_string(vndf_status status);

@@ -31,6 +31,7 @@ SYMBOLS = (
     "vndf_microbench", "vndf_sample_cap_reflect", "vndf_furnace", "vndf_pdf",
     "vndf_sample_cap_pdf_native", "vndf_histogram",
     "vndf_sample_cap_reflect_philox", "vndf_sample_heitz2018_reflect_philox",
+    "vndf_sample_cap_philox_host", "vndf_microbench_trace", "vndf_init",
 )
 
 
@@ -68,6 +69,9 @@ def lib() -> ctypes.CDLL:
         L.vndf_set_launch_config.argtypes = [i32, i32, i32]
         L.vndf_release_host_staging.argtypes = []
         L.vndf_microbench.argtypes = [i32, u64, i64, i32, P, P]
+        L.vndf_microbench_trace.argtypes = [i32, u64, i64, i32, P, P, P]
+        L.vndf_init.argtypes = [i32]
+        L.vndf_sample_cap_philox_host.argtypes = [u64, u64, i64, P, P, P, P, P]
         L.vndf_sample_cap_reflect.argtypes = [P] * 12 + [i64, P]
         for name in ("vndf_sample_cap_reflect_philox", "vndf_sample_heitz2018_reflect_philox"):
             getattr(L, name).argtypes = [u64, u64, i64, P, P, P, P, P, P]
@@ -283,6 +287,32 @@ def vndf_sample_cap_pdf_host(wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, h_x, h_
     _check("vndf_sample_cap_pdf_host", lib().vndf_sample_cap_pdf_host(*ptrs, n, st))
 
 
+def _host_ptr(a, n: int, name: str):
+    import numpy as np
+    import torch
+    if isinstance(a, torch.Tensor):
+        if a.is_cuda or a.dtype != torch.float32 or not a.is_contiguous() or a.numel() < n:
+            raise ValueError(f"{name}: expected a contiguous float32 CPU tensor of >= {n} elements")
+        return ctypes.c_void_p(a.data_ptr())
+    if isinstance(a, np.ndarray):
+        if a.dtype != np.float32 or not a.flags["C_CONTIGUOUS"] or a.size < n:
+            raise ValueError(f"{name}: expected a contiguous float32 array of >= {n} elements")
+        return ctypes.c_void_p(a.ctypes.data)
+    raise TypeError(f"{name}: expected a torch CPU tensor or numpy array")
+
+
+def vndf_sample_cap_philox_host(seed, first_index, n, h_x, h_y, h_z, pdf=None, stream=None):
+    """End-to-end config-4 call writing HOST buffers (CPU tensors, ideally
+    pinned: the kernel then writes them in place); blocking."""
+    import torch
+    n = int(n)
+    ptrs = [_host_ptr(a, n, nm) for a, nm in ((h_x, "h_x"), (h_y, "h_y"), (h_z, "h_z"))]
+    ptrs.append(_host_ptr(pdf, n, "pdf") if pdf is not None else None)
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream) if stream is None else _stream(stream, None)
+    _check("vndf_sample_cap_philox_host",
+           lib().vndf_sample_cap_philox_host(int(seed), int(first_index), n, *ptrs, st))
+
+
 def vndf_sample_cap_reflect(wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, wo_x, wo_y, wo_z, pdf, weight,
                             n=None, stream=None):
     """Appendix steps (1)-(2): reflected direction, Eq. 20 pdf, G2/G1 weight."""
@@ -348,6 +378,20 @@ def vndf_microbench(method, seed, lanes, iters, checksum, stream=None):
     p, dev = _dev_ptr(checksum, int(lanes), "checksum")
     _check("vndf_microbench", lib().vndf_microbench(int(method), int(seed), int(lanes), int(iters), p,
                                                     _stream(stream, dev)))
+
+
+def vndf_microbench_trace(method, seed, lanes, iters, checksum, trace, stream=None):
+    """NEXT-1 with every call recorded: trace (float32, >= 4 lanes iters) gets
+    (h.x, h.y, h.z, flag) per call, lane-major."""
+    p, dev = _dev_ptr(checksum, int(lanes), "checksum")
+    t, _ = _dev_ptr(trace, 4 * int(lanes) * int(iters), "trace", device=dev)
+    _check("vndf_microbench_trace", lib().vndf_microbench_trace(int(method), int(seed), int(lanes), int(iters),
+                                                                p, t, _stream(stream, dev)))
+
+
+def vndf_init(device: int = -1):
+    """Start libvndf's CUDA state on `device` now (vndf.h): later calls only enqueue."""
+    _check("vndf_init", lib().vndf_init(int(device)))
 
 
 def vndf_release_host_staging():

@@ -27,11 +27,27 @@ NVCC_FLAGS = [
 ]
 
 
+STAMP = LIB + ".srchash"
+
+
+def source_hash() -> str:
+    """SHA-256 of every source the library is built from plus the nvcc command
+    line: the build key (mtimes are unreliable across checkouts and copies)."""
+    import hashlib
+    h = hashlib.sha256()
+    h.update(" ".join([NVCC, *NVCC_FLAGS]).encode())
+    for p in sorted(DEPS):
+        h.update(os.path.basename(p).encode())
+        with open(p, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()
+
+
 def stale() -> bool:
-    if not os.path.exists(LIB):
+    if not (os.path.exists(LIB) and os.path.exists(STAMP)):
         return True
-    t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(p) > t for p in DEPS)
+    with open(STAMP) as f:
+        return f.read().strip() != source_hash()
 
 
 class _FileLock:
@@ -67,6 +83,8 @@ def _build_locked(force: bool, verbose: bool) -> str:
         if res.returncode != 0:
             raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
         os.replace(LIB + ".tmp", LIB)
+        with open(STAMP, "w") as f:
+            f.write(source_hash() + "\n")
         log = os.path.join(HERE, "csrc", "ptxas.log")
         with open(log, "w") as f:
             f.write(res.stderr)

@@ -1,6 +1,5 @@
 // kernels_common.cuh -- device helpers shared by the kernels: argument structs, streaming
-// vector loads/stores, programmatic dependent launch, TMA bulk copy, the
-// per-sample dispatch.
+// vector loads/stores, programmatic dependent launch, the per-sample dispatch.
 // Part of libvndf's single translation unit (included by vndf.cu inside its
 // anonymous namespace); see vndf.cu for the kernel list and DESIGN.md s.6.
 #pragma once
@@ -113,36 +112,6 @@ __device__ __forceinline__ void st_stream<8>(float* p, const Vec<8>& r) {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch_dependents() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
-
-// ------------------------------------------ TMA bulk copy into shared memory --
-// One elected thread arms an mbarrier with the expected byte count and issues
-// cp.async.bulk (global -> shared, SASS UBLKCP); every thread waits on the
-// barrier's phase 0.  `bytes` must be a multiple of 16, both addresses 16-byte
-// aligned.
-__device__ __forceinline__ void bulk_load_shared(void* smem_dst, const void* gmem_src, uint32_t bytes,
-                                                 uint64_t* bar) {
-    const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
-    const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
-    if (threadIdx.x == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                     ::"r"(d), "l"(gmem_src), "r"(bytes), "r"(b)
-                     : "memory");
-    }
-    uint32_t done = 0;
-    while (!done) {
-        asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}\n"
-            : "=r"(done)
-            : "r"(b)
-            : "memory");
-    }
 }
 
 // ------------------------------------------------------------ one sample --

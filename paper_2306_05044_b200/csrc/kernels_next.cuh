@@ -267,26 +267,29 @@ __global__ void __launch_bounds__(256) histogram_kernel(int mode, float wx, floa
 // ------------------------------------- NEXT-1: sampler-only microbenchmark --
 // The paper's GPU methodology: each lane calls Listing 1 `iters`
 // times.  Lane t draws its incidence and roughness once from the config-4
-// recipe (Philox block of index t).  Iteration k uses the integer Weyl
-// sequence u1 = u(s1 + k A1), u2 = u(s2 + k A2) (s1 = W0, s2 = W1) and then
-// rotates wi about z by a fixed angle with explicitly rounded fp32 operations
-// (so every call does the full Listing 1 -- nothing is loop-invariant -- and
-// the host oracle can replay the exact fp32 incidences).  h.x + 2 h.y + 3 h.z
-// is summed into a per-lane checksum (the sink).  No pdf, no flag, no fix-up.
-// VARIANT 0 = cap (production fp32 arithmetic), 1 = Heitz (Listing 2),
-// 2 = Listing 3 literal.
+// recipe (Philox blocks X, Y of index t).  Iteration k uses the integer Weyl
+// sequence u1 = u(s1 + k A1), u2 = u(s2 + k A2) (s1 = Y0, s2 = Y1, the words
+// of the recipe's u1, u2) and then rotates wi about z by a fixed angle with
+// explicitly rounded fp32 operations (so every call does the full Listing 1 --
+// nothing is loop-invariant -- and the host oracle can replay the exact fp32
+// incidences).  h.x + 2 h.y + 3 h.z is summed into a per-lane checksum (the
+// sink).  No pdf, no fix-up.  VARIANT 0 = cap (production fp32 arithmetic),
+// 1 = Heitz (Listing 2), 2 = Listing 3 literal.
+// TRACE (vndf_microbench_trace, tests only): also writes every call's
+// (h.x, h.y, h.z, flag) to trace[4 (t iters + k) ..], flag = the cap's
+// conditioning flag (1.0f: this call would be recomputed in float64 by the
+// production kernels; always 0 for variants 1 and 2).
 constexpr uint32_t kWeyl1 = 0x9E3779B9u, kWeyl2 = 0x7F4A7C15u;
 constexpr float kRotC = 0.764842187f, kRotS = 0.644217687f;  // cos, sin of 0.7 rad (fp32)
 
-template <int VARIANT>
+template <int VARIANT, bool TRACE>
 __global__ void __launch_bounds__(256) microbench_kernel(uint64_t seed, int64_t lanes, int iters,
-                                                         const float* __restrict__ gtab,
-                                                         float* __restrict__ checksum) {
+                                                         float* __restrict__ checksum, float4* __restrict__ trace) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= lanes) return;
-    const uint4 W = philox_sample(seed, (uint64_t)t);
-    const Inputs in = c4_inputs_fp32(W, gtab);
-    uint32_t x1 = W.x, x2 = W.y;
+    const uint4 X = philox_block(seed, (uint64_t)t, 0u), Y = philox_block(seed, (uint64_t)t, 1u);
+    const Inputs in = c4_inputs_fp32(X, Y);
+    uint32_t x1 = Y.x, x2 = Y.y;
     float wx = in.wx, wy = in.wy;
     float acc = 0.0f;
 #pragma unroll 4
@@ -294,14 +297,16 @@ __global__ void __launch_bounds__(256) microbench_kernel(uint64_t seed, int64_t 
         const float v1 = fmaf(fw(x1), 0x1p-24f, -0.5f);
         const float f2 = fw(x2);
         Sample o;
+        bool flag = false;
         if (VARIANT == 0) {
-            cap_fp32<false, kFrameUpper>(wx, wy, in.wz, in.ax, in.ay, v1, f2 * 0x1p-24f,
-                                   fmaf(f2, -0x1p-24f, 1.0f), o);
+            flag = cap_fp32<false, kFrameUpper>(wx, wy, in.wz, in.ax, in.ay, v1, f2 * 0x1p-24f,
+                                                fmaf(f2, -0x1p-24f, 1.0f), o);
         } else if (VARIANT == 1) {
             heitz_fp32<false, false>(wx, wy, in.wz, in.ax, in.ay, v1, f2 * 0x1p-24f, o);
         } else {
             cap_literal_fp32(wx, wy, in.wz, in.ax, in.ay, v1, f2 * 0x1p-24f, o);
         }
+        if (TRACE) trace[t * (int64_t)iters + k] = make_float4(o.x, o.y, o.z, flag ? 1.0f : 0.0f);
         acc += o.x + 2.0f * o.y + 3.0f * o.z;
         x1 += kWeyl1;
         x2 += kWeyl2;

@@ -16,33 +16,66 @@
 // ----------------------------------------------------- fused Philox kernel --
 // Deferred float64 fix-up queue of the fused kernel (compute-bound: inline
 // fp64 work would diverge the warp and its call would inflate the register
-// allocation).  Flagged local indices are appended with one (warp-aggregated)
-// atomic each (~0.4% of samples); a second kernel recomputes them with all
-// lanes busy.  If the queue overflowed (count > cap), the fix-up kernel
-// rescans every sample's flag instead: always correct, slower only then.
+// allocation).  Flagged local indices are appended with one atomicAdd per
+// flagged sample (~0.05% of the config-4 samples); a second kernel recomputes
+// them with all lanes busy.  If the queue overflowed (count > cap), the fix-up
+// kernel rescans every sample's flag instead: always correct, slower only then.
 
-// ctr = first + k, the Philox counter of local sample k
+// Config-4 inputs of Philox counter ctr (both blocks, SURVEY s.8(d)).
+template <bool FW_HI>
+__device__ __forceinline__ Inputs c4_inputs_ks(const PhiloxKeys& ks, uint64_t ctr) {
+    uint4 X, Y;
+    philox_pair_ks(ks, ctr, X, Y);
+    return c4_inputs_fp32<FW_HI>(X, Y);
+}
+
+__device__ __forceinline__ Inputs c4_inputs_seed(uint64_t seed, uint64_t ctr) {
+    return c4_inputs_fp32(philox_block(seed, ctr, 0u), philox_block(seed, ctr, 1u));
+}
+
+// Appends the flagged samples of a V-sample chunk (bit j of `bits`: local
+// index i + j) to the queue, warp-cooperatively: one ballot per position, one
+// atomicAdd per warp and position that has a flagged sample, slots by prefix
+// popcount.  No divergent branch: the sample loop keeps the Philox round keys
+// in uniform registers (a per-thread atomic inside the loop made ptxas move
+// them to regular registers, turning every round's key XOR into a 3-register
+// LOP3 at half issue rate).
+template <int V>
+__device__ __forceinline__ void queue_flags(const FixQueue& fq, unsigned bits, uint64_t i) {
+    const unsigned act = __activemask();
+    if (__any_sync(act, bits != 0u)) {
+        const unsigned lane = threadIdx.x & 31u;
+        const int leader = __ffs(act) - 1;
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            const bool f = (bits >> j) & 1u;
+            const unsigned m = __ballot_sync(act, f);
+            if (m) {
+                unsigned long long base = 0;
+                if ((int)lane == leader) base = atomicAdd(fq.count, (unsigned long long)__popc(m));
+                base = __shfl_sync(act, base, leader);
+                const unsigned long long slot = base + (unsigned long long)__popc(m & ((1u << lane) - 1u));
+                if (f && slot < fq.cap) fq.idx[slot] = i + (uint64_t)j;
+            }
+        }
+    }
+}
+
+// ctr = first + k, the Philox counter of local sample k; returns the
+// conditioning flag (always false for Heitz)
 template <int METHOD, bool PDF>
-__device__ __forceinline__ Sample philox_one(const PhiloxKeys& ks, uint64_t ctr, uint64_t k,
-                                             const FixQueue& fq, const float* __restrict__ tab) {
-    const Inputs in = c4_inputs_fp32<true, VNDF_CAP_FW_HI && METHOD == kCap>(philox_sample_ks(ks, ctr), tab);
-    Sample o;
+__device__ __forceinline__ bool philox_one(const PhiloxKeys& ks, uint64_t ctr, Sample& o) {
+    const Inputs in = c4_inputs_ks<VNDF_CAP_FW_HI && METHOD == kCap>(ks, ctr);
     if (METHOD == kCap) {
         // config-4 inputs are on the upper hemisphere (wi.z = 1 - u > 0): no flip
-        const bool flag = cap_fp32<PDF, kFrameUpper>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o);
-        if (__builtin_expect(flag, 0)) {
-            const unsigned long long slot = atomicAdd(fq.count, 1ull);
-            if (slot < fq.cap) fq.idx[slot] = k;
-        }
-    } else {
-        heitz_fp32<PDF, false>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, o);
+        return cap_fp32<PDF, kFrameUpper>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o);
     }
-    return o;
+    heitz_fp32<PDF, false>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, o);
+    return false;
 }
 
 __global__ void __launch_bounds__(128) philox_fixup_kernel(uint64_t seed, uint64_t first, int64_t n,
-                                                            FixQueue fq, const float* __restrict__ gtab,
-                                                            float* __restrict__ hx,
+                                                            FixQueue fq, float* __restrict__ hx,
                                                             float* __restrict__ hy, float* __restrict__ hz,
                                                             float* __restrict__ pdf) {
     const uint64_t count = *fq.count;
@@ -60,7 +93,7 @@ __global__ void __launch_bounds__(128) philox_fixup_kernel(uint64_t seed, uint64
         return;
     }
     for (uint64_t k = t0; k < (uint64_t)n; k += stride) {  // overflow: rescan
-        const Inputs in = c4_inputs_fp32(philox_sample(seed, first + k), gtab);
+        const Inputs in = c4_inputs_seed(seed, first + k);
         Sample o;
         if (cap_fp32<true, kFrameUpper>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o)) {
             const float4 f = cap_philox_fp64(seed, first + k);
@@ -72,19 +105,20 @@ __global__ void __launch_bounds__(128) philox_fixup_kernel(uint64_t seed, uint64
     }
 }
 
-// One block per SM, holding the SM's single copy of the 64 KB table: the cap
-// kernel with 640 threads (20 warps), the Heitz kernel with 1024 (32 warps,
-// <= 64 registers); both with 8 samples per thread (one 256-bit store per
-// output plane).  Swept on B200 (tools/build_variant.py + tools/variants.py)
-// over 256 x 3, 320-512 x 2 and 512-1024 x 1 blocks per SM and 2/4/8 samples
-// per thread: cap 184 (256 x 3, 4 per thread) -> 204 Gsamples/s, Heitz
-// 175 -> 186.5, together with the pipe-balance knobs VNDF_CAP_FW_HI and
-// VNDF_TABLE_IMAD.
+// Persistent grid (SMs x resident blocks); 8 samples per thread (one 256-bit
+// store per output plane).  Block sizes / resident blocks per SM are build
+// knobs swept on B200 (tools/build_variant.py + tools/variants.py).
 #ifndef VNDF_PHILOX_BLOCK_CAP
-#define VNDF_PHILOX_BLOCK_CAP 640
+#define VNDF_PHILOX_BLOCK_CAP 256
 #endif
 #ifndef VNDF_PHILOX_BLOCK_HEITZ
-#define VNDF_PHILOX_BLOCK_HEITZ 1024
+#define VNDF_PHILOX_BLOCK_HEITZ 256
+#endif
+#ifndef VNDF_PHILOX_MINB_CAP
+#define VNDF_PHILOX_MINB_CAP 1
+#endif
+#ifndef VNDF_PHILOX_MINB_HEITZ
+#define VNDF_PHILOX_MINB_HEITZ 1
 #endif
 #ifndef VNDF_PHILOX_V_CAP
 #define VNDF_PHILOX_V_CAP 8
@@ -95,22 +129,17 @@ __global__ void __launch_bounds__(128) philox_fixup_kernel(uint64_t seed, uint64
 template <int METHOD>
 struct PhiloxLaunch {
     static constexpr int kBlock = METHOD == kCap ? VNDF_PHILOX_BLOCK_CAP : VNDF_PHILOX_BLOCK_HEITZ;
+    static constexpr int kMinBlocks = METHOD == kCap ? VNDF_PHILOX_MINB_CAP : VNDF_PHILOX_MINB_HEITZ;
     static constexpr int kV = METHOD == kCap ? VNDF_PHILOX_V_CAP : VNDF_PHILOX_V_HEITZ;
 };
 
 // ALIGNED: first is a multiple of V, so the counters of a chunk share their
 // high word and differ only in the low bits (no 64-bit add per sample).
 template <int METHOD, bool PDF, int V, bool ALIGNED>
-__global__ void __launch_bounds__(PhiloxLaunch<METHOD>::kBlock, 1) philox_kernel(uint64_t seed, uint64_t first, int64_t n,
-                                                     float* __restrict__ hxp, float* __restrict__ hyp,
-                                                     float* __restrict__ hzp, float* __restrict__ pdfp,
-                                                     FixQueue fq, const float* __restrict__ gtab,
-                                                     const __grid_constant__ PhiloxKeys ks) {
-    // Stage the 64 KB sin/cos table of the incidence azimuth in shared memory
-    // with one TMA bulk copy (cp.async.bulk, completion on an mbarrier).
-    extern __shared__ __align__(16) float tab[];
-    __shared__ __align__(8) uint64_t tab_bar;
-    bulk_load_shared(tab, gtab, kSinTableBytes, &tab_bar);
+__global__ void __launch_bounds__(PhiloxLaunch<METHOD>::kBlock, PhiloxLaunch<METHOD>::kMinBlocks)
+    philox_kernel(uint64_t first, int64_t n, float* __restrict__ hxp, float* __restrict__ hyp,
+                  float* __restrict__ hzp, float* __restrict__ pdfp, FixQueue fq,
+                  const __grid_constant__ PhiloxKeys ks) {
     const int64_t nchunks = n / V;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -118,10 +147,12 @@ __global__ void __launch_bounds__(PhiloxLaunch<METHOD>::kBlock, 1) philox_kernel
         const int64_t i = c * V;
         const uint64_t base = first + (uint64_t)i;
         Vec<V> hx, hy, hz, pd;
+        unsigned flags = 0;
 #pragma unroll
         for (int j = 0; j < V; ++j) {
             const uint64_t ctr = ALIGNED ? (base | (uint64_t)j) : base + (uint64_t)j;
-            const Sample o = philox_one<METHOD, PDF>(ks, ctr, (uint64_t)(i + j), fq, tab);
+            Sample o;
+            flags |= (unsigned)philox_one<METHOD, PDF>(ks, ctr, o) << j;
             hx.v[j] = o.x;
             hy.v[j] = o.y;
             hz.v[j] = o.z;
@@ -131,15 +162,21 @@ __global__ void __launch_bounds__(PhiloxLaunch<METHOD>::kBlock, 1) philox_kernel
         st_stream<V>(hyp + i, hy);
         st_stream<V>(hzp + i, hz);
         if (PDF) st_stream<V>(pdfp + i, pd);
+        if (METHOD == kCap) queue_flags<V>(fq, flags, (uint64_t)i);
     }
     if (V > 1) {
         const int64_t i = nchunks * V + tid;
         if (i < n) {
-            const Sample o = philox_one<METHOD, PDF>(ks, first + (uint64_t)i, (uint64_t)i, fq, tab);
+            Sample o;
+            const bool f = philox_one<METHOD, PDF>(ks, first + (uint64_t)i, o);
             hxp[i] = o.x;
             hyp[i] = o.y;
             hzp[i] = o.z;
             if (PDF) pdfp[i] = o.pdf;
+            if (METHOD == kCap && f) {
+                const unsigned long long slot = atomicAdd(fq.count, 1ull);
+                if (slot < fq.cap) fq.idx[slot] = (uint64_t)i;
+            }
         }
     }
 }
@@ -154,29 +191,17 @@ struct ReflectOut {
 };
 
 template <int METHOD>
-__device__ __forceinline__ Reflected philox_reflect_one(const PhiloxKeys& ks, uint64_t ctr, uint64_t k,
-                                                        const FixQueue& fq, const float* __restrict__ tab) {
-    const Inputs in = c4_inputs_fp32<true, VNDF_CAP_FW_HI && METHOD == kCap>(philox_sample_ks(ks, ctr), tab);
-    Reflected r;
-    if (METHOD == kCap) {
-        const bool flag = cap_reflect_fp32<false>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, r);
-        if (__builtin_expect(flag, 0)) {
-            const unsigned long long slot = atomicAdd(fq.count, 1ull);
-            if (slot < fq.cap) fq.idx[slot] = k;
-        }
-    } else {
-        heitz_reflect_fp32<false>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, r);
-    }
-    return r;
+__device__ __forceinline__ bool philox_reflect_one(const PhiloxKeys& ks, uint64_t ctr, Reflected& r) {
+    const Inputs in = c4_inputs_ks<VNDF_CAP_FW_HI && METHOD == kCap>(ks, ctr);
+    if (METHOD == kCap) return cap_reflect_fp32<false>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, r);
+    heitz_reflect_fp32<false>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, r);
+    return false;
 }
 
 template <int METHOD, int V, bool ALIGNED>
-__global__ void __launch_bounds__(PhiloxLaunch<METHOD>::kBlock, 1)
-    philox_reflect_kernel(uint64_t first, int64_t n, ReflectOut out, FixQueue fq, const float* __restrict__ gtab,
+__global__ void __launch_bounds__(PhiloxLaunch<METHOD>::kBlock, PhiloxLaunch<METHOD>::kMinBlocks)
+    philox_reflect_kernel(uint64_t first, int64_t n, ReflectOut out, FixQueue fq,
                           const __grid_constant__ PhiloxKeys ks) {
-    extern __shared__ __align__(16) float tab[];
-    __shared__ __align__(8) uint64_t tab_bar;
-    bulk_load_shared(tab, gtab, kSinTableBytes, &tab_bar);
     const int64_t nchunks = n / V;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -184,10 +209,12 @@ __global__ void __launch_bounds__(PhiloxLaunch<METHOD>::kBlock, 1)
         const int64_t i = c * V;
         const uint64_t base = first + (uint64_t)i;
         Vec<V> ox, oy, oz, pd, wg;
+        unsigned flags = 0;
 #pragma unroll
         for (int j = 0; j < V; ++j) {
             const uint64_t ctr = ALIGNED ? (base | (uint64_t)j) : base + (uint64_t)j;
-            const Reflected r = philox_reflect_one<METHOD>(ks, ctr, (uint64_t)(i + j), fq, tab);
+            Reflected r;
+            flags |= (unsigned)philox_reflect_one<METHOD>(ks, ctr, r) << j;
             ox.v[j] = r.x;
             oy.v[j] = r.y;
             oz.v[j] = r.z;
@@ -199,23 +226,28 @@ __global__ void __launch_bounds__(PhiloxLaunch<METHOD>::kBlock, 1)
         st_stream<V>(out.oz + i, oz);
         st_stream<V>(out.pdf + i, pd);
         st_stream<V>(out.weight + i, wg);
+        if (METHOD == kCap) queue_flags<V>(fq, flags, (uint64_t)i);
     }
     if (V > 1) {
         const int64_t i = nchunks * V + tid;
         if (i < n) {
-            const Reflected r = philox_reflect_one<METHOD>(ks, first + (uint64_t)i, (uint64_t)i, fq, tab);
+            Reflected r;
+            const bool f = philox_reflect_one<METHOD>(ks, first + (uint64_t)i, r);
             out.ox[i] = r.x;
             out.oy[i] = r.y;
             out.oz[i] = r.z;
             out.pdf[i] = r.pdf;
             out.weight[i] = r.weight;
+            if (METHOD == kCap && f) {
+                const unsigned long long slot = atomicAdd(fq.count, 1ull);
+                if (slot < fq.cap) fq.idx[slot] = (uint64_t)i;
+            }
         }
     }
 }
 
 __global__ void __launch_bounds__(128) philox_reflect_fixup_kernel(uint64_t seed, uint64_t first, int64_t n,
-                                                                    FixQueue fq, const float* __restrict__ gtab,
-                                                                    ReflectOut out) {
+                                                                    FixQueue fq, ReflectOut out) {
     const uint64_t count = *fq.count;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -233,7 +265,7 @@ __global__ void __launch_bounds__(128) philox_reflect_fixup_kernel(uint64_t seed
         return;
     }
     for (uint64_t k = t0; k < (uint64_t)n; k += stride) {  // overflow: rescan
-        const Inputs in = c4_inputs_fp32(philox_sample(seed, first + k), gtab);
+        const Inputs in = c4_inputs_seed(seed, first + k);
         Reflected r;
         if (cap_reflect_fp32<false>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, r)) fix(k);
     }
@@ -274,7 +306,6 @@ __global__ void __launch_bounds__(256) count_stream_kernel(StreamArgs a, int64_t
 }
 
 __global__ void __launch_bounds__(256) count_philox_kernel(uint64_t seed, uint64_t first, int64_t n,
-                                                           const float* __restrict__ gtab,
                                                            unsigned long long* count) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t start = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -283,7 +314,7 @@ __global__ void __launch_bounds__(256) count_philox_kernel(uint64_t seed, uint64
         const int64_t i = start + r * stride;
         bool flag = false;
         if (i < n) {
-            const Inputs in = c4_inputs_fp32(philox_sample(seed, first + (uint64_t)i), gtab);
+            const Inputs in = c4_inputs_seed(seed, first + (uint64_t)i);
             Sample o;
             flag = cap_fp32<true, kFrameUpper>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o);
         }

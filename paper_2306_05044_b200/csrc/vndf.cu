@@ -155,8 +155,15 @@ cudaError_t grid_for(const void* kernel, int block, int64_t work_items, int* gri
 std::map<int, cudaMemPool_t> g_pools;
 
 cudaError_t queue_alloc(void** p, size_t bytes, cudaStream_t s) {
+    // Inside a stream capture the allocation becomes a graph memory node;
+    // creating a pool there is illegal (tools/capture_probe.cu), so a captured
+    // call allocates from the device's default pool instead.
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaError_t e = cudaStreamIsCapturing(s, &cs);
+    if (e != cudaSuccess) return e;
+    if (cs != cudaStreamCaptureStatusNone) return cudaMallocAsync(p, bytes, s);
     int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
+    e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     cudaMemPool_t pool = nullptr;
     {
@@ -172,7 +179,9 @@ cudaError_t queue_alloc(void** p, size_t bytes, cudaStream_t s) {
         props.location.id = dev;
         e = cudaMemPoolCreate(&pool, &props);
         if (e != cudaSuccess) return e;
-        uint64_t thr = UINT64_MAX;
+        // keep up to 256 MB reserved between calls (a 2^30-sample fused
+        // call's queue is 64 MB); vndf_release_host_staging trims to zero
+        uint64_t thr = (uint64_t)256 << 20;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
         std::lock_guard<std::mutex> lk(g_mu);
         auto it = g_pools.find(dev);
@@ -184,54 +193,6 @@ cudaError_t queue_alloc(void** p, size_t bytes, cudaStream_t s) {
         }
     }
     return cudaMallocFromPoolAsync(p, bytes, pool, s);
-}
-
-// Opt a kernel into > 48 KB of dynamic shared memory, once per (device, kernel):
-// function attributes are per device, a process may drive several.
-std::map<std::pair<int, const void*>, bool> g_smem_attr;
-
-cudaError_t allow_dynamic_smem(const void* kernel, size_t bytes) {
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return e;
-    std::lock_guard<std::mutex> lk(g_mu);
-    const auto key = std::make_pair(dev, kernel);
-    if (g_smem_attr.count(key)) return cudaSuccess;
-    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    if (e == cudaSuccess) g_smem_attr[key] = true;
-    return e;
-}
-
-// Quadrant table sin(2 pi j / 2^16), j = 0 .. 16384, for the config-4
-// incidence azimuth: built on the host in float64 (correctly rounded to fp32),
-// uploaded once per device, kept for the life of the process (64 KB).
-std::map<int, float*> g_sin_tab;
-
-cudaError_t sincos_table(float** out) {
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return e;
-    std::lock_guard<std::mutex> lk(g_mu);
-    auto it = g_sin_tab.find(dev);
-    if (it != g_sin_tab.end()) {
-        *out = it->second;
-        return cudaSuccess;
-    }
-    std::vector<float> h(kSinTableEntries);
-    for (int j = 0; j < kSinTableEntries; ++j) {
-        const int jj = j < 16385 ? j : 16384;  // padding entries repeat the last one
-        h[j] = (float)sin(2.0 * 3.14159265358979323846 * (double)jj / 65536.0);
-    }
-    float* d = nullptr;
-    e = cudaMalloc((void**)&d, h.size() * sizeof(float));
-    if (e == cudaSuccess) e = cudaMemcpy(d, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) {
-        if (d) cudaFree(d);
-        return e;
-    }
-    g_sin_tab[dev] = d;
-    *out = d;
-    return cudaSuccess;
 }
 
 int block_size(int dflt = 256) {
@@ -349,11 +310,8 @@ vndf_status launch_philox_v(uint64_t seed, uint64_t first, int64_t n, float* hx,
                             float* pdf, cudaStream_t s) {
     const void* k = (const void*)philox_kernel<METHOD, PDF, V, ALIGNED>;
     const int block = block_size(PhiloxLaunch<METHOD>::kBlock);
-    const size_t smem = kSinTableBytes;
-    cudaError_t e = allow_dynamic_smem(k, smem);
-    if (e != cudaSuccess) return cuda_fail(e);
     int grid = 0;
-    e = grid_for(k, block, std::max<int64_t>(n / V, 1), &grid, true, smem);
+    cudaError_t e = grid_for(k, block, std::max<int64_t>(n / V, 1), &grid, true);
     if (e != cudaSuccess) return cuda_fail(e);
     FixQueue fq{nullptr, nullptr, 0};
     void* qbuf = nullptr;
@@ -371,14 +329,7 @@ vndf_status launch_philox_v(uint64_t seed, uint64_t first, int64_t n, float* hx,
             return cuda_fail(e);
         }
     }
-    float* gtab = nullptr;
-    e = sincos_table(&gtab);
-    if (e != cudaSuccess) {
-        if (qbuf) cudaFreeAsync(qbuf, s);
-        return cuda_fail(e);
-    }
-    philox_kernel<METHOD, PDF, V, ALIGNED><<<grid, block, smem, s>>>(seed, first, n, hx, hy, hz, pdf, fq, gtab,
-                                                            philox_keys(seed));
+    philox_kernel<METHOD, PDF, V, ALIGNED><<<grid, block, 0, s>>>(first, n, hx, hy, hz, pdf, fq, philox_keys(seed));
     e = cudaGetLastError();
     if (e == cudaSuccess && METHOD == kCap) {
         // one thread per queue slot up to SMs x 32 blocks; blocks past the
@@ -387,7 +338,7 @@ vndf_status launch_philox_v(uint64_t seed, uint64_t first, int64_t n, float* hx,
         e = sm_count(&sms);
         const int64_t fix_blocks = std::min<int64_t>(((int64_t)fq.cap + 127) / 128, (int64_t)std::max(sms, 1) * 32);
         if (e == cudaSuccess) {
-            philox_fixup_kernel<<<(int)fix_blocks, 128, 0, s>>>(seed, first, n, fq, gtab, hx, hy, hz, pdf);
+            philox_fixup_kernel<<<(int)fix_blocks, 128, 0, s>>>(seed, first, n, fq, hx, hy, hz, pdf);
             e = cudaGetLastError();
         }
     }
@@ -424,11 +375,8 @@ vndf_status launch_philox_reflect_v(uint64_t seed, uint64_t first, int64_t n, co
                                     cudaStream_t s) {
     const void* k = (const void*)philox_reflect_kernel<METHOD, V, ALIGNED>;
     const int block = block_size(PhiloxLaunch<METHOD>::kBlock);
-    const size_t smem = kSinTableBytes;
-    cudaError_t e = allow_dynamic_smem(k, smem);
-    if (e != cudaSuccess) return cuda_fail(e);
     int grid = 0;
-    e = grid_for(k, block, std::max<int64_t>(n / V, 1), &grid, true, smem);
+    cudaError_t e = grid_for(k, block, std::max<int64_t>(n / V, 1), &grid, true);
     if (e != cudaSuccess) return cuda_fail(e);
     FixQueue fq{nullptr, nullptr, 0};
     void* qbuf = nullptr;
@@ -445,20 +393,14 @@ vndf_status launch_philox_reflect_v(uint64_t seed, uint64_t first, int64_t n, co
             return cuda_fail(e);
         }
     }
-    float* gtab = nullptr;
-    e = sincos_table(&gtab);
-    if (e != cudaSuccess) {
-        if (qbuf) cudaFreeAsync(qbuf, s);
-        return cuda_fail(e);
-    }
-    philox_reflect_kernel<METHOD, V, ALIGNED><<<grid, block, smem, s>>>(first, n, out, fq, gtab, philox_keys(seed));
+    philox_reflect_kernel<METHOD, V, ALIGNED><<<grid, block, 0, s>>>(first, n, out, fq, philox_keys(seed));
     e = cudaGetLastError();
     if (e == cudaSuccess && METHOD == kCap) {
         int sms = 0;
         e = sm_count(&sms);
         const int64_t fix_blocks = std::min<int64_t>(((int64_t)fq.cap + 127) / 128, (int64_t)std::max(sms, 1) * 32);
         if (e == cudaSuccess) {
-            philox_reflect_fixup_kernel<<<(int)fix_blocks, 128, 0, s>>>(seed, first, n, fq, gtab, out);
+            philox_reflect_fixup_kernel<<<(int)fix_blocks, 128, 0, s>>>(seed, first, n, fq, out);
             e = cudaGetLastError();
         }
     }
@@ -579,6 +521,35 @@ void release_staging(Staging* sg) {
     destroy_staging(sg);
 }
 
+// The device of a call is the device of its stream (vndf.h): the per-device
+// caches (SM count, occupancy, memory pool, staging) key on the current
+// device, so an entry point makes the stream's device current for its
+// duration and restores the caller's afterwards.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(cudaStream_t s) {
+        int dev = 0, cur = 0;
+        // cudaStreamGetDevice is illegal inside a stream capture
+        // (tools/capture_probe.cu); a capturing caller has made its device
+        // current (the capture itself is bound to it).
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+            cudaGetLastError();
+            return;
+        }
+        if (cudaStreamGetDevice(s, &dev) != cudaSuccess) {
+            cudaGetLastError();  // an invalid stream is reported by the launch itself
+            return;
+        }
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != dev && cudaSetDevice(dev) == cudaSuccess) prev = cur;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+    DeviceGuard(const DeviceGuard&) = delete;
+    DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
 }  // namespace
 
 // ================================================================== C ABI ==
@@ -588,6 +559,7 @@ vndf_status vndf_sample_cap(const float* wi_x, const float* wi_y, const float* w
                             const float* alpha_x, const float* alpha_y, const float* u1,
                             const float* u2, float* h_x, float* h_y, float* h_z, int64_t n,
                             vndf_stream_t stream) {
+    DeviceGuard device_guard((cudaStream_t)stream);
     const StreamArgs a = make_args(wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, h_x, h_y, h_z, nullptr);
     vndf_status st = validate_stream(a, false, n);
     if (st != VNDF_OK || n == 0) return st;
@@ -598,6 +570,7 @@ vndf_status vndf_sample_cap_pdf(const float* wi_x, const float* wi_y, const floa
                                 const float* alpha_x, const float* alpha_y, const float* u1,
                                 const float* u2, float* h_x, float* h_y, float* h_z, float* pdf,
                                 int64_t n, vndf_stream_t stream) {
+    DeviceGuard device_guard((cudaStream_t)stream);
     const StreamArgs a = make_args(wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, h_x, h_y, h_z, pdf);
     vndf_status st = validate_stream(a, true, n);
     if (st != VNDF_OK || n == 0) return st;
@@ -608,6 +581,7 @@ vndf_status vndf_sample_cap_pdf_native(const float* wi_x, const float* wi_y, con
                                        const float* alpha_x, const float* alpha_y, const float* u1,
                                        const float* u2, float* h_x, float* h_y, float* h_z, float* pdf,
                                        int64_t n, vndf_stream_t stream) {
+    DeviceGuard device_guard((cudaStream_t)stream);
     const StreamArgs a = make_args(wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, h_x, h_y, h_z, pdf);
     vndf_status st = validate_stream(a, false, n);
     if (st != VNDF_OK || n == 0) return st;
@@ -619,6 +593,7 @@ vndf_status vndf_sample_heitz2018(const float* wi_x, const float* wi_y, const fl
                                   const float* alpha_x, const float* alpha_y, const float* u1,
                                   const float* u2, float* h_x, float* h_y, float* h_z, float* pdf,
                                   int64_t n, vndf_stream_t stream) {
+    DeviceGuard device_guard((cudaStream_t)stream);
     const StreamArgs a = make_args(wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, h_x, h_y, h_z, pdf);
     vndf_status st = validate_stream(a, false, n);
     if (st != VNDF_OK || n == 0) return st;
@@ -628,16 +603,19 @@ vndf_status vndf_sample_heitz2018(const float* wi_x, const float* wi_y, const fl
 
 vndf_status vndf_sample_cap_philox(uint64_t seed, uint64_t first_index, int64_t n, float* h_x,
                                    float* h_y, float* h_z, float* pdf, vndf_stream_t stream) {
+    DeviceGuard device_guard((cudaStream_t)stream);
     return launch_philox<kCap>(seed, first_index, n, h_x, h_y, h_z, pdf, (cudaStream_t)stream);
 }
 
 vndf_status vndf_sample_heitz2018_philox(uint64_t seed, uint64_t first_index, int64_t n, float* h_x,
                                          float* h_y, float* h_z, float* pdf, vndf_stream_t stream) {
+    DeviceGuard device_guard((cudaStream_t)stream);
     return launch_philox<kHeitz>(seed, first_index, n, h_x, h_y, h_z, pdf, (cudaStream_t)stream);
 }
 
 vndf_status vndf_philox4x32_10(uint64_t seed, uint64_t first_index, int64_t n, uint32_t block,
                                uint32_t* words, vndf_stream_t stream) {
+    DeviceGuard device_guard((cudaStream_t)stream);
     if (n < 0 || !words || !aligned(words, 16)) return VNDF_ERR_INVALID_ARGUMENT;
     if (n == 0) return VNDF_OK;
     int grid = 0;
@@ -652,6 +630,7 @@ vndf_status vndf_philox4x32_10(uint64_t seed, uint64_t first_index, int64_t n, u
 vndf_status vndf_count_fixups(const float* wi_x, const float* wi_y, const float* wi_z,
                               const float* alpha_x, const float* alpha_y, const float* u1,
                               const float* u2, int64_t n, uint64_t* count, vndf_stream_t stream) {
+    DeviceGuard device_guard((cudaStream_t)stream);
     if (n < 0 || !count || !aligned(count, 8)) return VNDF_ERR_INVALID_ARGUMENT;
     const void* in[7] = {wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2};
     for (auto p : in)
@@ -669,16 +648,13 @@ vndf_status vndf_count_fixups(const float* wi_x, const float* wi_y, const float*
 
 vndf_status vndf_count_fixups_philox(uint64_t seed, uint64_t first_index, int64_t n, uint64_t* count,
                                      vndf_stream_t stream) {
+    DeviceGuard device_guard((cudaStream_t)stream);
     if (n < 0 || !count || !aligned(count, 8)) return VNDF_ERR_INVALID_ARGUMENT;
     if (n == 0) return VNDF_OK;
     int grid = 0;
     cudaError_t e = grid_for((const void*)count_philox_kernel, 256, n, &grid);
     if (e != cudaSuccess) return cuda_fail(e);
-    float* gtab = nullptr;
-    e = sincos_table(&gtab);
-    if (e != cudaSuccess) return cuda_fail(e);
-    count_philox_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(seed, first_index, n, gtab,
-                                                                 (unsigned long long*)count);
+    count_philox_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(seed, first_index, n, (unsigned long long*)count);
     e = cudaGetLastError();
     return e == cudaSuccess ? VNDF_OK : cuda_fail(e);
 }
@@ -706,6 +682,7 @@ vndf_status vndf_sample_cap_pdf_host(const float* wi_x, const float* wi_y, const
                                      const float* alpha_x, const float* alpha_y, const float* u1,
                                      const float* u2, float* h_x, float* h_y, float* h_z, float* pdf,
                                      int64_t n, vndf_stream_t stream) {
+    DeviceGuard device_guard((cudaStream_t)stream);
     const StreamArgs host = make_args(wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, h_x, h_y, h_z, pdf);
     vndf_status st = validate_stream(host, true, n);
     if (st != VNDF_OK || n == 0) return st;
@@ -769,6 +746,62 @@ vndf_status vndf_sample_cap_pdf_host(const float* wi_x, const float* wi_y, const
     return e == cudaSuccess ? VNDF_OK : cuda_fail(e);
 }
 
+vndf_status vndf_sample_cap_philox_host(uint64_t seed, uint64_t first_index, int64_t n, float* h_x, float* h_y,
+                                        float* h_z, float* pdf, vndf_stream_t stream) {
+    DeviceGuard device_guard((cudaStream_t)stream);
+    vndf_status st = validate_philox_out(n, h_x, h_y, h_z, pdf);
+    if (st != VNDF_OK || n == 0) return st;
+    cudaStream_t user = (cudaStream_t)stream;
+    float* hout[4] = {h_x, h_y, h_z, pdf};
+    const int nout = pdf ? 4 : 3;
+    // Zero-copy: mapped page-locked outputs are written by the kernel across
+    // the host link in place (16 B per sample device -> host, nothing in).
+    {
+        void* dp[4] = {nullptr, nullptr, nullptr, nullptr};
+        bool mapped = true;
+        for (int k = 0; k < nout && mapped; ++k) mapped = (dp[k] = (void*)mapped_pointer(hout[k])) != nullptr;
+        if (mapped) {
+            st = launch_philox<kCap>(seed, first_index, n, (float*)dp[0], (float*)dp[1], (float*)dp[2],
+                                     (float*)dp[3], user);
+            if (st != VNDF_OK) return st;
+            const cudaError_t es = cudaStreamSynchronize(user);
+            return es == cudaSuccess ? VNDF_OK : cuda_fail(es);
+        }
+    }
+    // Otherwise: chunks through device staging, kernel then device -> host
+    // copies, round-robin over the staging streams.  With pageable outputs
+    // each copy completes before the next call returns, so chunks do not
+    // overlap their copies (pin the outputs for the zero-copy path above).
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e);
+    Staging* sg = nullptr;
+    e = acquire_staging(dev, &sg);
+    if (e != cudaSuccess) return cuda_fail(e);
+    vndf_status result = VNDF_OK;
+    e = cudaEventRecord(sg->ev[0], user);
+    for (int k = 0; k < kStagingSets && e == cudaSuccess; ++k) e = cudaStreamWaitEvent(sg->s[k], sg->ev[0], 0);
+    for (int64_t off = 0, c = 0; off < n && e == cudaSuccess && result == VNDF_OK; off += kStagingChunk, ++c) {
+        const int64_t m = std::min<int64_t>(kStagingChunk, n - off);
+        cudaStream_t s = sg->s[c % kStagingSets];
+        float* base = sg->buf + (size_t)(c % kStagingSets) * 11 * kStagingChunk;
+        float* d[4];
+        for (int k = 0; k < 4; ++k) d[k] = base + (size_t)(7 + k) * kStagingChunk;
+        result = launch_philox<kCap>(seed, first_index + (uint64_t)off, m, d[0], d[1], d[2], pdf ? d[3] : nullptr, s);
+        for (int k = 0; k < nout && e == cudaSuccess && result == VNDF_OK; ++k)
+            e = cudaMemcpyAsync(hout[k] + off, d[k], (size_t)m * sizeof(float), cudaMemcpyDeviceToHost, s);
+    }
+    for (int k = 0; k < kStagingSets; ++k) {
+        cudaEventRecord(sg->ev[1 + k], sg->s[k]);
+        cudaStreamWaitEvent(user, sg->ev[1 + k], 0);
+    }
+    const cudaError_t es = cudaStreamSynchronize(user);
+    if (e == cudaSuccess) e = es;
+    release_staging(sg);
+    if (result != VNDF_OK) return result;
+    return e == cudaSuccess ? VNDF_OK : cuda_fail(e);
+}
+
 vndf_status vndf_release_host_staging(void) {
     std::lock_guard<std::mutex> lk(g_mu);
     cudaError_t first = cudaSuccess;
@@ -781,6 +814,16 @@ vndf_status vndf_release_host_staging(void) {
         if (first == cudaSuccess) first = e;
     }
     g_staging.clear();
+    // return the fix-up queues' reserved pool memory (after pending frees)
+    for (auto& kv : g_pools) {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(kv.first);
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e == cudaSuccess) e = cudaMemPoolTrimTo(kv.second, 0);
+        cudaSetDevice(cur);
+        if (first == cudaSuccess) first = e;
+    }
     return first == cudaSuccess ? VNDF_OK : cuda_fail(first);
 }
 
@@ -788,6 +831,7 @@ vndf_status vndf_sample_cap_reflect(const float* wi_x, const float* wi_y, const 
                                     const float* alpha_x, const float* alpha_y, const float* u1,
                                     const float* u2, float* wo_x, float* wo_y, float* wo_z, float* pdf,
                                     float* weight, int64_t n, vndf_stream_t stream) {
+    DeviceGuard device_guard((cudaStream_t)stream);
     if (n < 0) return VNDF_ERR_INVALID_ARGUMENT;
     const void* in[7] = {wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2};
     const void* out[5] = {wo_x, wo_y, wo_z, pdf, weight};
@@ -833,12 +877,14 @@ vndf_status vndf_sample_cap_reflect(const float* wi_x, const float* wi_y, const 
 vndf_status vndf_sample_cap_reflect_philox(uint64_t seed, uint64_t first_index, int64_t n, float* wo_x,
                                            float* wo_y, float* wo_z, float* pdf, float* weight,
                                            vndf_stream_t stream) {
+    DeviceGuard device_guard((cudaStream_t)stream);
     return launch_philox_reflect<kCap>(seed, first_index, n, wo_x, wo_y, wo_z, pdf, weight, (cudaStream_t)stream);
 }
 
 vndf_status vndf_sample_heitz2018_reflect_philox(uint64_t seed, uint64_t first_index, int64_t n, float* wo_x,
                                                  float* wo_y, float* wo_z, float* pdf, float* weight,
                                                  vndf_stream_t stream) {
+    DeviceGuard device_guard((cudaStream_t)stream);
     return launch_philox_reflect<kHeitz>(seed, first_index, n, wo_x, wo_y, wo_z, pdf, weight,
                                          (cudaStream_t)stream);
 }
@@ -846,6 +892,7 @@ vndf_status vndf_sample_heitz2018_reflect_philox(uint64_t seed, uint64_t first_i
 vndf_status vndf_pdf(const float* h_x, const float* h_y, const float* h_z, const float* wi_x,
                      const float* wi_y, const float* wi_z, const float* alpha_x, const float* alpha_y,
                      float* pdf, int64_t n, vndf_stream_t stream) {
+    DeviceGuard device_guard((cudaStream_t)stream);
     if (n < 0 || !pdf || !aligned(pdf, 4)) return VNDF_ERR_INVALID_ARGUMENT;
     const void* in[8] = {h_x, h_y, h_z, wi_x, wi_y, wi_z, alpha_x, alpha_y};
     for (auto p : in) {
@@ -882,6 +929,7 @@ vndf_status vndf_pdf(const float* h_x, const float* h_y, const float* h_z, const
 vndf_status vndf_furnace(int method, float wi_x, float wi_y, float wi_z, float alpha_x, float alpha_y,
                          uint64_t seed, uint64_t first_index, int64_t n, double* sums,
                          vndf_stream_t stream) {
+    DeviceGuard device_guard((cudaStream_t)stream);
     if (n < 0 || !sums || !aligned(sums, 8) || (method != 0 && method != 1)) return VNDF_ERR_INVALID_ARGUMENT;
     cudaStream_t s = (cudaStream_t)stream;
     if (n == 0) {
@@ -914,6 +962,7 @@ vndf_status vndf_furnace(int method, float wi_x, float wi_y, float wi_z, float a
 vndf_status vndf_histogram(int method, int mode, float wi_x, float wi_y, float wi_z, float alpha_x,
                            float alpha_y, uint64_t seed, uint64_t first_index, int64_t n, int nt, int nphi,
                            uint64_t* counts, vndf_stream_t stream) {
+    DeviceGuard device_guard((cudaStream_t)stream);
     if (n < 0 || !counts || !aligned(counts, 8) || method < 0 || method > 2 || (mode != 0 && mode != 1) ||
         nt < 1 || nphi < 1 || (int64_t)nt * nphi > 8192)
         return VNDF_ERR_INVALID_ARGUMENT;
@@ -943,6 +992,7 @@ vndf_status vndf_histogram(int method, int mode, float wi_x, float wi_y, float w
 
 vndf_status vndf_microbench(int method, uint64_t seed, int64_t lanes, int iters, float* checksum,
                             vndf_stream_t stream) {
+    DeviceGuard device_guard((cudaStream_t)stream);
     if (lanes < 0 || iters < 0 || !checksum || !aligned(checksum, 4) || method < 0 || method > 2)
         return VNDF_ERR_INVALID_ARGUMENT;
     if (lanes == 0) return VNDF_OK;
@@ -950,15 +1000,59 @@ vndf_status vndf_microbench(int method, uint64_t seed, int64_t lanes, int iters,
     const int64_t grid = (lanes + block - 1) / block;
     if (grid > INT32_MAX) return VNDF_ERR_INVALID_ARGUMENT;
     cudaStream_t s = (cudaStream_t)stream;
-    float* gtab = nullptr;
-    cudaError_t e = sincos_table(&gtab);
-    if (e != cudaSuccess) return cuda_fail(e);
     switch (method) {
-        case 0: microbench_kernel<0><<<(int)grid, block, 0, s>>>(seed, lanes, iters, gtab, checksum); break;
-        case 1: microbench_kernel<1><<<(int)grid, block, 0, s>>>(seed, lanes, iters, gtab, checksum); break;
-        default: microbench_kernel<2><<<(int)grid, block, 0, s>>>(seed, lanes, iters, gtab, checksum); break;
+        case 0: microbench_kernel<0, false><<<(int)grid, block, 0, s>>>(seed, lanes, iters, checksum, nullptr); break;
+        case 1: microbench_kernel<1, false><<<(int)grid, block, 0, s>>>(seed, lanes, iters, checksum, nullptr); break;
+        default: microbench_kernel<2, false><<<(int)grid, block, 0, s>>>(seed, lanes, iters, checksum, nullptr); break;
     }
-    e = cudaGetLastError();
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? VNDF_OK : cuda_fail(e);
+}
+
+vndf_status vndf_microbench_trace(int method, uint64_t seed, int64_t lanes, int iters, float* checksum,
+                                  float* trace, vndf_stream_t stream) {
+    DeviceGuard device_guard((cudaStream_t)stream);
+    if (lanes < 0 || iters < 0 || !checksum || !aligned(checksum, 4) || !trace || !aligned(trace, 16) ||
+        method < 0 || method > 2)
+        return VNDF_ERR_INVALID_ARGUMENT;
+    if (lanes == 0) return VNDF_OK;
+    if (overlaps(checksum, trace, 4 * lanes * (int64_t)iters * (int64_t)sizeof(float)) ||
+        overlaps(trace, checksum, lanes * (int64_t)sizeof(float)))
+        return VNDF_ERR_INVALID_ARGUMENT;
+    const int block = 256;
+    const int64_t grid = (lanes + block - 1) / block;
+    if (grid > INT32_MAX) return VNDF_ERR_INVALID_ARGUMENT;
+    cudaStream_t s = (cudaStream_t)stream;
+    float4* t = (float4*)trace;
+    switch (method) {
+        case 0: microbench_kernel<0, true><<<(int)grid, block, 0, s>>>(seed, lanes, iters, checksum, t); break;
+        case 1: microbench_kernel<1, true><<<(int)grid, block, 0, s>>>(seed, lanes, iters, checksum, t); break;
+        default: microbench_kernel<2, true><<<(int)grid, block, 0, s>>>(seed, lanes, iters, checksum, t); break;
+    }
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? VNDF_OK : cuda_fail(e);
+}
+
+vndf_status vndf_init(int device) {
+    int cur = 0;
+    cudaError_t e = cudaGetDevice(&cur);
+    if (e != cudaSuccess) return cuda_fail(e);
+    const int dev = device < 0 ? cur : device;
+    if (dev != cur && (e = cudaSetDevice(dev)) != cudaSuccess) return cuda_fail(e);
+    // the runtime's one-time initialisation (module load) happens here, then
+    // the per-device caches and the fix-up queue pool
+    int sms = 0;
+    e = sm_count(&sms);
+    // touching one kernel loads libvndf's module into the context (the load
+    // is what waits for queued device work; later per-kernel loads do not:
+    // tools/first_call_probe.py)
+    cudaFuncAttributes fa;
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, (const void*)philox_words_kernel);
+    void* q = nullptr;
+    if (e == cudaSuccess) e = queue_alloc(&q, 256, cudaStreamPerThread);
+    if (e == cudaSuccess) e = cudaFreeAsync(q, cudaStreamPerThread);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(cudaStreamPerThread);
+    if (dev != cur) cudaSetDevice(cur);
     return e == cudaSuccess ? VNDF_OK : cuda_fail(e);
 }
 

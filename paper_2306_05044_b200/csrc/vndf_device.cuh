@@ -479,12 +479,13 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
     return c;
 }
 
-// Config-4 inputs from ONE Philox4x32-10 block per sample (counter = sample
-// index, key = seed; vndf.h, DESIGN.md s.5).  The 128 bits are split as
-//   u1 = W0[31:8] 2^-24, u2 = W1[31:8] 2^-24                 (the method's uniforms)
-//   ax = 0.01 * 100^(W2[31:8] 2^-24), ay = 0.01 * 100^(W3[31:8] 2^-24)
-//   ua = (W0[7:0] | W1[7:0] << 8) 2^-16, ub = (W2[7:0] | W3[7:0] << 8) 2^-16
-//   wi: z = 1 - ua, r = sqrt(ua (2 - ua)), phi = 2 pi ub   (uniform upper hemisphere)
+// Config-4 inputs from TWO Philox4x32-10 blocks per sample (counter = sample
+// index, key = seed, vndf.h, DESIGN.md s.5 reading R12):
+//   X = Philox(ctr (i_lo, i_hi, 0, 0)), Y = Philox(ctr (i_lo, i_hi, 1, 0))
+//   wi: z = 1 - u(X0), r = sqrt(u(X0) (2 - u(X0))), phi = 2 pi u(X1)  (uniform upper hemisphere)
+//   ax = 0.01 * 100^u(X2), ay = 0.01 * 100^u(X3)                      (log-uniform [0.01, 1])
+//   u1 = u(Y0), u2 = u(Y1)                                            (the method's uniforms)
+// with u(w) = (w >> 8) 2^-24 (24 bits each).
 constexpr float kLog2_100F = 6.64385618977472436f;
 constexpr double kLog2_100D = 6.64385618977472436;
 
@@ -494,7 +495,6 @@ struct Inputs {
     float wx, wy, wz, ax, ay, v1, u2, q;
 };
 
-// The 24-bit integer of a word, as float: u(w) = fw(w) 2^-24 exactly.
 // Integer multiply-add / high multiply pinned to IMAD (FMA pipe): left to
 // itself the compiler turns x * 2^k + c into SHF/IADD3/LEA on the ALU pipe.
 __device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
@@ -508,16 +508,13 @@ __device__ __forceinline__ uint32_t imad_hi(uint32_t a, uint32_t b) {
     return d;
 }
 
+// The 24-bit integer of a word, as float: u(w) = fw(w) 2^-24 exactly.
 __device__ __forceinline__ float fw(uint32_t w) { return __uint2float_rn(w >> 8); }
 // The same value with the shift as a high multiply (FMA-heavy pipe, see imad),
 // for kernels short of ALU-pipe issue (VNDF_CAP_FW_HI).
 __device__ __forceinline__ float fw_hi(uint32_t w) { return __uint2float_rn(imad_hi(w, 1u << 24)); }
 template <bool HI>
 __device__ __forceinline__ float fw_t(uint32_t w) { return HI ? fw_hi(w) : fw(w); }
-// The 16-bit integer made of the low bytes of two words, as float.
-__device__ __forceinline__ float fw16(uint32_t lo, uint32_t hi) {
-    return __uint2float_rn(__byte_perm(lo, hi, 0x7740) & 0xFFFFu);
-}
 
 // The per-round Philox keys of a seed, precomputed on the host and passed as a
 // __grid_constant__ kernel parameter: the round XORs then read them from the
@@ -538,93 +535,87 @@ inline PhiloxKeys philox_keys(uint64_t seed) {
     return ks;
 }
 
-__device__ __forceinline__ uint4 philox_sample_ks(const PhiloxKeys& ks, uint64_t i) {
-    uint4 c = make_uint4((uint32_t)i, (uint32_t)(i >> 32), 0u, 0u);
-#pragma unroll
-    for (int r = 0; r < 10; ++r) {
-        uint32_t hi0, lo0, hi1, lo1;
-        mul_hilo(0xD2511F53u, c.x, hi0, lo0);
-        mul_hilo(0xCD9E8D57u, c.z, hi1, lo1);
-        c = make_uint4(hi1 ^ c.y ^ ks.k0[r], lo1, hi0 ^ c.w ^ ks.k1[r], lo0);
-    }
-    return c;
+// One Philox round in plain C (no inline asm), so that the compiler folds the
+// constant counter words (c.z = block, c.w = 0) and shares the rounds that the
+// two blocks of one sample have in common: both blocks multiply the same
+// c.x in round 0, and their states differ in one word after it.
+__device__ __forceinline__ uint4 philox_round(uint4 c, uint32_t k0, uint32_t k1) {
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c.x;
+    const uint64_t p1 = (uint64_t)0xCD9E8D57u * c.z;
+    return make_uint4((uint32_t)(p1 >> 32) ^ c.y ^ k0, (uint32_t)p1, (uint32_t)(p0 >> 32) ^ c.w ^ k1,
+                      (uint32_t)p0);
 }
 
-__device__ __forceinline__ uint4 philox_sample(uint64_t seed, uint64_t i) {
-    return philox4x32_10(make_uint4((uint32_t)i, (uint32_t)(i >> 32), 0u, 0u),
+// Blocks 0 and 1 of sample counter i with the precomputed keys.
+__device__ __forceinline__ void philox_pair_ks(const PhiloxKeys& ks, uint64_t i, uint4& X, uint4& Y) {
+    uint4 x = make_uint4((uint32_t)i, (uint32_t)(i >> 32), 0u, 0u);
+    uint4 y = make_uint4((uint32_t)i, (uint32_t)(i >> 32), 1u, 0u);
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        x = philox_round(x, ks.k0[r], ks.k1[r]);
+        y = philox_round(y, ks.k0[r], ks.k1[r]);
+    }
+    X = x;
+    Y = y;
+}
+
+__device__ __forceinline__ uint4 philox_block(uint64_t seed, uint64_t i, uint32_t block) {
+    return philox4x32_10(make_uint4((uint32_t)i, (uint32_t)(i >> 32), block, 0u),
                          make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
 }
 
-// sin and cos of 2 pi K / 2^16 for a 16-bit K (bits 16-31 of K are ignored)
-// from the quadrant table S[j] = sin(2 pi j / 2^16), j = 0 .. 2^14 (correctly
-// rounded fp32, built on the host in float64), using cos(x) = sin(pi/2 - x):
-// with r = K mod 2^14 and j = r (even quadrant) or 2^14 - r (odd quadrant),
-// sin = +-S[j], cos = +-S[2^14 - j]; the signs are the quadrant's, applied to
-// the sign bit.  Exact reduction, ~0.5 ulp: relative accuracy in each
-// component.  Two LDS.32 replace the octant table's four swap/sign selects; the
-// index and sign arithmetic can be pinned to IMAD (VNDF_TABLE_IMAD) for kernels
-// short of ALU-pipe issue (profiles/r1/prof_c4_r1_summary.txt).
-constexpr int kSinTableEntries = 16388;  // 16385 used, padded to a 16-byte multiple
-constexpr unsigned kSinTableBytes = kSinTableEntries * sizeof(float);
-// Index and sign arithmetic of the table lookup: 1 = pinned to IMAD (FMA-heavy
-// pipe), 0 = the compiler's SHF/IADD3/SEL (ALU pipe).  1 won with three
-// 256-thread blocks per SM; with one block per SM (FMA-heavy pipe the busier)
-// 0 is faster: cap +1.1%, Heitz +2.8% (tools/variants.py).
-#ifndef VNDF_TABLE_IMAD
-#define VNDF_TABLE_IMAD 0
-#endif
+// Block 0 only (furnace and histogram kernels: u1 = u(W0), u2 = u(W1)).
+__device__ __forceinline__ uint4 philox_sample(uint64_t seed, uint64_t i) { return philox_block(seed, i, 0u); }
 
-// 2^16 as a constant-bank value: a literal power-of-two multiplier is
-// strength-reduced to SHF/IADD3 (ALU pipe) even through mad.lo.
-__constant__ uint32_t kImad2e16 = 65536u;
-
-__device__ __forceinline__ void sincos_2pi_u16(uint32_t K, const float* __restrict__ S, float* s,
-                                               float* c) {
-    const uint32_t r = K & 0x3FFFu;
-#if VNDF_TABLE_IMAD
-    const uint32_t odd = imad_hi(K & 0x4000u, 1u << 18);        // bit 14 of K
-    const uint32_t js = imad(odd, imad(r, 0xFFFFFFFEu, 16384u), r);  // r or 2^14 - r
-    const float a = S[js], b = S[16384u - js];
-    const uint32_t m16 = kImad2e16;
-    *s = __uint_as_float(__float_as_uint(a) ^ (imad(K, m16, 0u) & 0x80000000u));           // q = 2, 3
-    *c = __uint_as_float(__float_as_uint(b) ^ (imad(K, m16, 0x40000000u) & 0x80000000u));  // q = 1, 2
-#else
-    const uint32_t js = (K & 0x4000u) ? 16384u - r : r;  // r or 2^14 - r
-    const float a = S[js], b = S[16384u - js];
-    *s = __uint_as_float(__float_as_uint(a) ^ ((K << 16) & 0x80000000u));             // q = 2, 3
-    *c = __uint_as_float(__float_as_uint(b) ^ (((K + 0x4000u) << 16) & 0x80000000u));  // q = 1, 2
-#endif
+// sin and cos of phi = 2 pi u(w) for the 24-bit uniform of a word, with
+// relative accuracy in each component (the incidence needs it: the stretch
+// multiplies an absolute error of wi.x, wi.y by up to max(a)/|M^-1 wi|, large
+// at grazing incidence; MUFU.SIN/COS, absolute error 2^-21.4, would not do).
+// Exact integer reduction: with k = w >> 8 and r the low 22 bits of k read as
+// a signed number (r in [-2^21, 2^21)), k = q 2^22 + r and
+//   phi = q pi/2 + theta,  theta = 2 pi r 2^-24,  |theta| <= pi/4;
+// r 2^10 is the int32 (w & ~0xFF) << 2, converted exactly; theta takes one
+// rounding.  sin/cos(theta) by fp32 polynomials fitted for relative error on
+// [0, pi/4] (tools/sincos_fit.py: <= 1.95 / 1.44 ulp over all 2^22 reduced
+// arguments); the quadrant q = (k + 2^21) >> 22 swaps them (q odd) and sets
+// the signs: sin negative for q = 2, 3; cos negative for q = 1, 2.
+__device__ __forceinline__ void sincos_2pi_u24(uint32_t w, float* s, float* c) {
+    const int32_t ir = (int32_t)((w & 0xFFFFFF00u) << 2);             // r 2^10
+    const float th = __int2float_rn(ir) * 0x1.921fb6p-32f;             // 2 pi 2^-34 (fp32)
+    const float x = th * th;
+    float ps = fmaf(x, -1.951729937e-04f, 8.332177997e-03f);
+    ps = fmaf(x, ps, -1.666665524e-01f);
+    const float sn = fmaf(th * x, ps, th);
+    float pc = fmaf(x, 2.438356933e-05f, -1.388668199e-03f);
+    pc = fmaf(x, pc, 4.166661948e-02f);
+    pc = fmaf(x, pc, -0.5f);
+    const float cs = fmaf(x, pc, 1.0f);
+    const uint32_t q0 = w + 0x20000000u;   // bits 31:30 = q
+    const uint32_t q1 = w + 0x60000000u;   // bits 31:30 = q + 1
+    const bool odd = (q0 & 0x40000000u) != 0u;
+    const float a = odd ? cs : sn, b = odd ? sn : cs;
+    *s = __uint_as_float(__float_as_uint(a) ^ (q0 & 0x80000000u));
+    *c = __uint_as_float(__float_as_uint(b) ^ (q1 & 0x80000000u));
 }
 
-// tab = nullptr: sincospif; else the 16-bit table (shared or global memory).
-// (A compile-time switch: the product kernels always pass the table.)
 // FW_HI: convert the 24-bit uniforms with fw_hi (bit-identical to fw).
-template <bool TABLE = true, bool FW_HI = false>
-__device__ __forceinline__ Inputs c4_inputs_fp32(uint4 W, const float* __restrict__ tab) {
+template <bool FW_HI = false>
+__device__ __forceinline__ Inputs c4_inputs_fp32(uint4 X, uint4 Y) {
     Inputs in;
-    const float fa = fw16(W.x, W.y);
-    const float ua = fa * 0x1p-16f;
-    const float z = fmaf(fa, -0x1p-16f, 1.0f);          // 1 - ua, exact
+    const float fa = fw_t<FW_HI>(X.x);
+    const float ua = fa * 0x1p-24f;
+    const float z = fmaf(fa, -0x1p-24f, 1.0f);          // 1 - ua, exact
     const float r = sqrt_approx(ua * (1.0f + z));       // sqrt(ua (2 - ua))
-    // wi needs RELATIVE accuracy in each component: the stretch multiplies an
-    // absolute error of wi.x, wi.y by up to max(a)/|M^-1 wi|, which is large at
-    // grazing incidence.  sincospif (exact reduction in units of pi, ~1 ulp)
-    // or the correctly rounded 16-bit table give that; MUFU.SIN/COS (absolute
-    // error 2^-21.4) would not.
     float sp, cp;
-    if (TABLE) {
-        sincos_2pi_u16(__byte_perm(W.z, W.w, 0x7740), tab, &sp, &cp);
-    } else {
-        sincospif(fw16(W.z, W.w) * 0x1p-15f, &sp, &cp);  // 2 pi ub, ub = fw16 2^-16
-    }
+    sincos_2pi_u24(X.y, &sp, &cp);
     in.wx = r * cp;
     in.wy = r * sp;
     in.wz = z;
     // 0.01 * 100^u = 2^((u - 1) log2 100); u log2 100 = fw (2^-24 log2 100) exactly
-    in.ax = ex2_approx(fmaf(fw_t<FW_HI>(W.z), kLog2_100F * 0x1p-24f, -kLog2_100F));
-    in.ay = ex2_approx(fmaf(fw_t<FW_HI>(W.w), kLog2_100F * 0x1p-24f, -kLog2_100F));
-    in.v1 = fmaf(fw_t<FW_HI>(W.x), 0x1p-24f, -0.5f);
-    const float f2 = fw_t<FW_HI>(W.y);
+    in.ax = ex2_approx(fmaf(fw_t<FW_HI>(X.z), kLog2_100F * 0x1p-24f, -kLog2_100F));
+    in.ay = ex2_approx(fmaf(fw_t<FW_HI>(X.w), kLog2_100F * 0x1p-24f, -kLog2_100F));
+    in.v1 = fmaf(fw_t<FW_HI>(Y.x), 0x1p-24f, -0.5f);
+    const float f2 = fw_t<FW_HI>(Y.y);
     in.u2 = f2 * 0x1p-24f;
     in.q = fmaf(f2, -0x1p-24f, 1.0f);
     return in;
@@ -632,35 +623,38 @@ __device__ __forceinline__ Inputs c4_inputs_fp32(uint4 W, const float* __restric
 
 __device__ __forceinline__ double u01d(uint32_t w) { return (double)(w >> 8) * 0x1p-24; }
 
-// The config-4 inputs of a Philox block in double from the exact uniforms:
+// The config-4 inputs of a sample in double from the exact uniforms:
 // in = (wi.x, wi.y, wi.z, alpha_x, alpha_y, u1, u2) (vndf.h recipe).
-__device__ __forceinline__ void c4_inputs_fp64(uint4 W, double in[7]) {
-    const double ua = (double)((W.x & 0xFFu) | ((W.y & 0xFFu) << 8)) * 0x1p-16;
-    const double ub = (double)((W.z & 0xFFu) | ((W.w & 0xFFu) << 8)) * 0x1p-16;
+__device__ __forceinline__ void c4_inputs_fp64(uint4 X, uint4 Y, double in[7]) {
+    const double ua = u01d(X.x);
     const double r = sqrt(ua * (2.0 - ua));
     double sp, cp;
-    sincospi(2.0 * ub, &sp, &cp);
+    sincospi(2.0 * u01d(X.y), &sp, &cp);
     in[0] = r * cp;
     in[1] = r * sp;
     in[2] = 1.0 - ua;
-    in[3] = exp2((u01d(W.z) - 1.0) * kLog2_100D);
-    in[4] = exp2((u01d(W.w) - 1.0) * kLog2_100D);
-    in[5] = u01d(W.x);
-    in[6] = u01d(W.y);
+    in[3] = exp2((u01d(X.z) - 1.0) * kLog2_100D);
+    in[4] = exp2((u01d(X.w) - 1.0) * kLog2_100D);
+    in[5] = u01d(Y.x);
+    in[6] = u01d(Y.y);
 }
 
-// Float64 fix-up for a config-4 sample: regenerate the word, build the inputs
+__device__ __forceinline__ void c4_inputs_fp64(uint64_t seed, uint64_t i, double in[7]) {
+    c4_inputs_fp64(philox_block(seed, i, 0u), philox_block(seed, i, 1u), in);
+}
+
+// Float64 fix-up for a config-4 sample: regenerate the words, build the inputs
 // in double from the exact uniforms, sample in double.
 __device__ __noinline__ float4 cap_philox_fp64(uint64_t seed, uint64_t i) {
     double in[7];
-    c4_inputs_fp64(philox_sample(seed, i), in);
+    c4_inputs_fp64(seed, i, in);
     return cap_fp64_d(in[0], in[1], in[2], in[3], in[4], in[5], in[6]);
 }
 
 // The same for the reflection outputs (wo.xyz, Eq. 20 pdf, G2/G1 weight).
 __device__ __noinline__ void cap_reflect_philox_fp64(uint64_t seed, uint64_t i, double out[5]) {
     double in[7];
-    c4_inputs_fp64(philox_sample(seed, i), in);
+    c4_inputs_fp64(seed, i, in);
     cap_reflect_fp64_d(in[0], in[1], in[2], in[3], in[4], in[5], in[6], out);
 }
 

@@ -94,6 +94,14 @@ def test_argument_validation_without_gpu(vndf):
     assert L.vndf_count_fixups_philox(1, 0, 4, None, None) == INV
     assert L.vndf_sample_cap_pdf_host(*P, -1, None) == INV
     assert L.vndf_sample_cap_pdf_host(*P, 0, None) == vndf.VNDF_OK
+    assert L.vndf_sample_cap_philox_host(1, 0, -1, *P[7:11], None) == INV
+    assert L.vndf_sample_cap_philox_host(1, 0, 0, *P[7:11], None) == vndf.VNDF_OK
+    assert L.vndf_sample_cap_philox_host(1, 0, 8, None, *P[8:11], None) == INV
+    assert L.vndf_sample_cap_philox_host(1, 0, 8, P[7], P[7], P[9], P[10], None) == INV
+    assert L.vndf_microbench_trace(0, 1, -1, 64, P[0], P[1], None) == INV
+    assert L.vndf_microbench_trace(0, 1, 16, 64, P[0], None, None) == INV
+    assert L.vndf_microbench_trace(3, 1, 16, 64, P[0], P[1], None) == INV
+    assert L.vndf_microbench_trace(0, 1, 0, 64, P[0], P[1], None) == vndf.VNDF_OK
     # NEXT rows
     assert L.vndf_sample_cap_reflect(*P, P[0], -1, None) == INV
     assert L.vndf_sample_cap_reflect(*P[:11], None, 16, None) == INV          # weight required

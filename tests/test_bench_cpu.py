@@ -1,6 +1,7 @@
-"""bench.py's host-side pieces on the CPU: the roofline objects (HBM, issue and
-instruction-mix bounds) carry the contract's keys and consistent arithmetic,
-and the CPU baseline times the oracle as it stands (bounded sample)."""
+"""bench.py's host-side pieces on the CPU: the roofline objects (HBM and issue
+bounds) carry the contract's keys and consistent arithmetic, and the CPU
+baseline times the oracle as it stands (bounded samples) and checks GPU-side
+outputs against it (here: the oracle's own outputs, so zero error)."""
 import numpy as np
 import pytest
 
@@ -21,19 +22,29 @@ def test_hbm_roofline_keys_and_arithmetic(bench):
     assert r["traffic"] is None or r["traffic"] > 0
 
 
-def test_issue_and_mix_rooflines(bench):
-    r = bench.issue_roofline(200.0, "cap_philox_c4_warp_inst_per_sample")
-    assert r["bound"] == "alu" and r["unit"] == "Gsamples/s"
-    ipc = float(r["model"].split("/ ")[1].split()[0])
-    assert r["peak"] == pytest.approx(148 * 4 * 1.965e9 / ipc / 1e9, rel=1e-3)
-    m = bench.mix_roofline(200.0)
-    assert m["peak"] < r["peak"]  # the measured-rate bound is tighter than 1 inst/clk
-    assert m["frac"] == pytest.approx(200.0 / m["peak"], rel=1e-3)
+def test_issue_roofline(bench):
+    r = bench.issue_roofline(150.0, "cap_philox_c4_warp_inst_per_sample")
+    assert r is not None
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert k in r
+    assert r["bound"] == "alu" and r["unit"] == "Gwarp-inst/s"
+    assert r["peak"] == pytest.approx(148 * 4 * 1.965, rel=1e-4)
+    assert r["achieved"] == pytest.approx(150.0 * r["warp_inst_per_sample"], rel=1e-3)
+    assert r["frac"] == pytest.approx(r["achieved"] / r["peak"], rel=1e-3)
+    assert r["gsamples_s_bound"] == pytest.approx(r["peak"] / r["warp_inst_per_sample"], rel=1e-3)
 
 
 def test_cpu_baseline_is_the_oracle(bench, orc):
     import synth
-    x = synth.fill_numpy(2, 1, 1 << 12)
-    r = bench.cpu_baseline([x[k] for k in synth.PLANES], 1 << 12, budget_s=0.3)
+    idx = np.arange(5, 5 + 512, dtype=np.uint64)
+    h, p, _ = orc.batch_sample_philox(orc.CAP, bench.C4_SEED, idx)
+    x1 = synth.fill_numpy(1, 0, 1 << 10)
+    x3 = synth.fill_numpy(3, 2, 1 << 12)
+    r = bench.cpu_baseline(check=(idx, h.astype(np.float32), p.astype(np.float32)),
+                           c1_planes=[x1[k] for k in synth.PLANES], c3_planes=[x3[k] for k in synth.PLANES],
+                           budget_s=0.3, log2_sub=12)
     assert r["kind"] == "oracle" and r["cores"] >= 1 and r["value"] > 0
-    assert r["value_1_thread"] > 0 and "samples" in r["sample"]
+    for k in ("c4_2e24", "c1_2e16", "c3_2e24"):
+        assert r["subranges"][k]["T_threads"] > 0 and r["subranges"][k]["1_thread"] > 0
+    pv = r["parity_vs_gpu"]
+    assert pv["samples"] == 512 and pv["over_tol"] == 0 and pv["max_abs_dh"] < 1e-6

@@ -1,29 +1,73 @@
 """NEXT-1: the sampler-only microbenchmark kernels (the paper's GPU methodology,
-P:814-817) compute what the float64 oracle replays: per-lane checksums of 64
-Listing-1 calls (vndf.h vndf_microbench).  No fix-up runs here, so rare
-ill-conditioned samples may exceed the per-sample tolerance; the checksum of a
-lane is 64 samples x (1 + 2 + 3) weights, so the bound is 64 * 6 * 2e-5."""
+P:814-817: Listing 1 called 64 times per lane) compute what the float64 oracle
+replays, call by call: vndf_microbench_trace records every call's h (and the
+cap's conditioning flag), compared element by element with the oracle's
+replay of the same Weyl sequence and fp32 incidence rotation
+(orc_batch_microbench_trace).  The microbenchmark runs no fix-up, so the
+spherical-cap calls the flag marks (the production kernels recompute those in
+float64) are exempt and counted; every other cap call must meet the 2e-5
+contract.  The literal fp32 Listings (2 and 3) carry no such guarantee
+(readings R7, R8): they are held to the per-call tolerance on >= 99% of calls.
+The checksums of vndf_microbench (the timed kernel) are the sums of exactly
+these calls."""
 import numpy as np
 import pytest
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
+TOL_H = 2e-5
 
-@pytest.mark.parametrize("method", [0, 1, 2], ids=["cap", "heitz", "cap_literal"])
-def test_microbench_checksums_match_oracle(method):
+
+@pytest.fixture(scope="module")
+def env():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import __graft_entry__
     __graft_entry__.build()
     import oracle
     import paper_2306_05044_b200 as vndf
-    lanes, iters = 1 << 14, 64
-    out = torch.empty(lanes, dtype=torch.float32, device="cuda:0")
-    vndf.vndf_microbench(method, 11, lanes, iters, out)
+    return oracle, vndf
+
+
+@pytest.mark.parametrize("method", [0, 1, 2], ids=["cap", "heitz", "cap_literal"])
+def test_microbench_every_call_matches_oracle(env, method):
+    oracle, vndf = env
+    lanes, iters = 4096, 64
+    ck = torch.empty(lanes, dtype=torch.float32, device="cuda:0")
+    tr = torch.empty(lanes * iters * 4, dtype=torch.float32, device="cuda:0")
+    vndf.vndf_microbench_trace(method, 11, lanes, iters, ck, tr)
     torch.cuda.synchronize()
-    ref = oracle.batch_microbench(method, 11, lanes, iters)
-    err = np.abs(out.cpu().numpy().astype(np.float64) - ref)
-    bound = iters * 6 * 2e-5
-    assert np.median(err) < 1e-4
-    assert (err <= bound).mean() >= (0.999 if method == 0 else 0.99), (err <= bound).mean()
+    got = tr.cpu().numpy().reshape(lanes, iters, 4).astype(np.float64)
+    ref = oracle.batch_microbench_trace(method, 11, lanes, iters)
+    err = np.abs(got[..., :3] - ref).max(axis=2)
+    flag = got[..., 3] != 0.0
+    ok = err <= TOL_H
+    print(f"method {method}: max |dh| {err.max():.2e} (unflagged {err[~flag].max():.2e}), "
+          f"flagged {flag.mean():.2e}, within 2e-5 {ok.mean():.6f}")
+    if method == 0:
+        assert flag.mean() < 5e-3
+        assert err[~flag].max() <= TOL_H, float(err[~flag].max())
+    else:
+        assert not flag.any()
+        assert ok.mean() >= 0.99
+        assert np.median(err) < 1e-6
+    # the timed kernel's checksum is the sum of exactly these calls (fp32 sum)
+    s = (got[..., 0] + 2 * got[..., 1] + 3 * got[..., 2]).sum(axis=1)
+    np.testing.assert_allclose(ck.cpu().numpy().astype(np.float64), s, atol=2e-4)
+
+
+@pytest.mark.parametrize("method", [0, 1, 2], ids=["cap", "heitz", "cap_literal"])
+def test_microbench_checksum_kernel_equals_trace_kernel(env, method):
+    """vndf_microbench (timed) and vndf_microbench_trace run the same calls:
+    the same checksums (to fp32 contraction differences of the sink) at the
+    bench's lane count scale."""
+    oracle, vndf = env
+    lanes, iters = 1 << 16, 64
+    a = torch.empty(lanes, dtype=torch.float32, device="cuda:0")
+    b = torch.empty(lanes, dtype=torch.float32, device="cuda:0")
+    tr = torch.empty(lanes * iters * 4, dtype=torch.float32, device="cuda:0")
+    vndf.vndf_microbench(method, 5, lanes, iters, a)
+    vndf.vndf_microbench_trace(method, 5, lanes, iters, b, tr)
+    torch.cuda.synchronize()
+    torch.testing.assert_close(a, b, rtol=1e-5, atol=1e-4)

@@ -321,6 +321,30 @@ def test_host_entry_point_matches_device(env):
         np.testing.assert_array_equal(a.cpu().numpy(), b)
 
 
+def test_philox_host_entry_point_matches_device(env):
+    """vndf_sample_cap_philox_host (config-4 end to end, host outputs) is bit
+    identical to vndf_sample_cap_philox: pinned (zero-copy), pageable (staged
+    chunks, ragged), and without pdf."""
+    oracle, vndf, synth, dev = env
+    n = (1 << 22) + 2 ** 21 + 13     # three staging chunks, ragged
+    first = 2**32 - 1000             # the 32-bit counter carry inside the call
+    d = vndf.empty_outputs(n, dev)
+    vndf.vndf_sample_cap_philox(3, first, n, *d)
+    ref = [t.cpu() for t in d]
+    hp = [torch.empty(n, dtype=torch.float32).pin_memory() for _ in range(4)]
+    vndf.vndf_sample_cap_philox_host(3, first, n, *hp)
+    for a, b in zip(ref, hp):
+        assert torch.equal(a, b)
+    nu = [np.empty(n, dtype=np.float32) for _ in range(4)]
+    vndf.vndf_sample_cap_philox_host(3, first, n, *nu)
+    for a, b in zip(ref, nu):
+        np.testing.assert_array_equal(a.numpy(), b)
+    h3 = [np.empty(n, dtype=np.float32) for _ in range(3)]
+    vndf.vndf_sample_cap_philox_host(3, first, n, *h3)
+    for a, b in zip(ref[:3], h3):
+        np.testing.assert_array_equal(a.numpy(), b)
+
+
 def test_fixup_rates(env):
     """The float64 fix-up stays rare (it is the accuracy safety net, DESIGN.md s.6)."""
     oracle, vndf, synth, dev = env
@@ -380,10 +404,11 @@ def test_heitz_philox_conditioned_parity(env):
     idx = np.arange(77, 77 + n, dtype=np.uint64)
     h_ref, p_ref, ti = oracle.batch_sample_philox(oracle.HEITZ, 3, idx)
     eh, ep = _errors([o.cpu().numpy() for o in out[:3]], out[3].cpu().numpy(), h_ref, p_ref)
-    W = oracle.philox_words(3, idx, 0).astype(np.uint64)
-    ax = 0.01 * 100.0 ** ((W[:, 2] >> 8) / 2**24)
-    ay = 0.01 * 100.0 ** ((W[:, 3] >> 8) / 2**24)
-    u1, u2 = (W[:, 0] >> 8) / 2**24, (W[:, 1] >> 8) / 2**24
+    X = oracle.philox_words(3, idx, 0).astype(np.uint64)   # wi, alpha
+    Y = oracle.philox_words(3, idx, 1).astype(np.uint64)   # u1, u2
+    ax = 0.01 * 100.0 ** ((X[:, 2] >> 8) / 2**24)
+    ay = 0.01 * 100.0 ** ((X[:, 3] >> 8) / 2**24)
+    u1, u2 = (Y[:, 0] >> 8) / 2**24, (Y[:, 1] >> 8) / 2**24
     N = 1.0 / np.sqrt((h_ref[0] / ax) ** 2 + (h_ref[1] / ay) ** 2 + h_ref[2] ** 2)
     rim = 1.0 - u2 * np.cos(2 * np.pi * u1) ** 2
     with np.errstate(divide="ignore"):

@@ -1,8 +1,8 @@
 """Loose performance floors (well below the measured values in BASELINE.md s.4)
 so that a silent slow path -- scalar accesses, a lost vector path, a fallback
 of any kind -- fails the suite instead of only the bench: the config-2 step
->= 5.5 TB/s (measured 6.9), the fused config-4 kernel >= 150 Gsamples/s at
-2^28 (measured ~204), the end-to-end host path >= 1.0 Gsamples/s (1.72)."""
+>= 5.5 TB/s (measured 6.9), the fused config-4 kernel >= 120 Gsamples/s at
+2^28 (two Philox blocks per sample), the end-to-end host path >= 1.0 Gsamples/s (1.72)."""
 import time
 
 import pytest
@@ -49,7 +49,7 @@ def test_floors(env):
     o = vndf.empty_outputs(n, dev)
     ms = _time(lambda: vndf.vndf_sample_cap_philox(3, 0, n, *o), 5)
     gs = n / ms / 1e6
-    assert gs >= 150, f"fused config 4 at {gs:.1f} Gsamples/s"
+    assert gs >= 120, f"fused config 4 at {gs:.1f} Gsamples/s"
     del o
     torch.cuda.empty_cache()
 
