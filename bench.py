@@ -256,6 +256,16 @@ def issue_roofline(gsamples_s: float, key: str, n_per_launch: int = None, launch
            "warp_inst_per_sample": inst, "gsamples_s_bound": round(peak / inst, 2),
            "model": f"{SMS} SMs x {SMSPS_PER_SM} SMSPs x 1 warp-inst/clk x {SM_MAX_MHZ:.0f} MHz; "
                     f"{inst} warp-inst/sample (ncu sm__inst_executed / samples)"}
+    # the FMA datapath: IMAD.WIDE.U32 (Philox) holds it ~4.3 clk per warp-instruction
+    # and does not overlap with FP32 FFMA/FMUL on B200 (tools/mix_probe.cu), so the
+    # sum of the measured per-instruction costs bounds the kernel (DESIGN.md s.6.4)
+    cyc = _profiled(key.replace("warp_inst_per_sample", "fma_pipe_cycles_per_warp_sample"))
+    if cyc:
+        bound = SMS * SMSPS_PER_SM * f * 32 / cyc / 1e9
+        out["fma_pipe"] = {"cycles_per_warp_sample": cyc, "gsamples_s_bound": round(bound, 2),
+                           "frac": round(gsamples_s / bound, 4),
+                           "model": "IMAD.WIDE 4.335 clk + FP32 FMA-pipe instruction 1.03 clk + IMAD 2 clk "
+                                    "per warp-instruction (measured), ncu dynamic counts per sample"}
     return out
 
 

@@ -13,6 +13,7 @@ struct FixQueue {
     unsigned long long* count;
     uint64_t* idx;
     uint64_t cap;
+    unsigned bcap;  // shared-memory block queue slots used (fused kernels, <= kBlockQueue)
 };
 
 struct StreamArgs {

@@ -33,31 +33,72 @@ __device__ __forceinline__ Inputs c4_inputs_seed(uint64_t seed, uint64_t ctr) {
     return c4_inputs_fp32(philox_block(seed, ctr, 0u), philox_block(seed, ctr, 1u));
 }
 
+// Block-level fix-up queue of the fused kernels.  Flagged local indices are
+// collected in shared memory (a warp reserves its slots with one shared-memory
+// atomic) and published to the global queue once per block at the end of the
+// kernel (one global atomic per block).  A global atomic per flagged warp-chunk
+// instead (round 1) stalled the warp on the ~L2 round trip of its return value
+// in the ~12% of warp-chunks that hold a flagged sample: 8% of the kernel's
+// time at config 4 (tools/fused_ablation.cu).  Samples past the block's slots
+// go to the global queue directly (correct, slower: a persistent block meets
+// ~1.8k flagged samples at 2^30 samples per call, so only calls far larger
+// than config 4 reach it; test hook VNDF_DEBUG_BLOCK_QUEUE).
+constexpr int kBlockQueue = 4096;
+struct BlockQueue {
+    uint64_t idx[kBlockQueue];
+    unsigned count;
+    unsigned long long base;
+};
+
+__device__ __forceinline__ void block_queue_init(BlockQueue& bq) {
+    if (threadIdx.x == 0) bq.count = 0u;
+    __syncthreads();
+}
+
 // Appends the flagged samples of a V-sample chunk (bit j of `bits`: local
-// index i + j) to the queue, warp-cooperatively: one ballot per position, one
-// atomicAdd per warp and position that has a flagged sample, slots by prefix
-// popcount.  No divergent branch: the sample loop keeps the Philox round keys
-// in uniform registers (a per-thread atomic inside the loop made ptxas move
-// them to regular registers, turning every round's key XOR into a 3-register
-// LOP3 at half issue rate).
-template <int V>
-__device__ __forceinline__ void queue_flags(const FixQueue& fq, unsigned bits, uint64_t i) {
+// index i + j), warp-cooperatively: the branch is warp-uniform (no divergent
+// branch in the sample loop, so ptxas keeps the Philox round keys in uniform
+// registers), one shared atomic per warp reserves the warp's slots, lanes
+// place their samples by an exclusive prefix sum of their counts.
+__device__ __forceinline__ void queue_flags(const FixQueue& fq, BlockQueue& bq, unsigned bits, uint64_t i) {
     const unsigned act = __activemask();
-    if (__any_sync(act, bits != 0u)) {
-        const unsigned lane = threadIdx.x & 31u;
-        const int leader = __ffs(act) - 1;
+    if (!__any_sync(act, bits != 0u)) return;
+    const unsigned lane = threadIdx.x & 31u;
+    const int leader = __ffs(act) - 1;
+    const unsigned c = (unsigned)__popc(bits);
+    unsigned incl = c;  // inclusive prefix sum over the active lanes
 #pragma unroll
-        for (int j = 0; j < V; ++j) {
-            const bool f = (bits >> j) & 1u;
-            const unsigned m = __ballot_sync(act, f);
-            if (m) {
-                unsigned long long base = 0;
-                if ((int)lane == leader) base = atomicAdd(fq.count, (unsigned long long)__popc(m));
-                base = __shfl_sync(act, base, leader);
-                const unsigned long long slot = base + (unsigned long long)__popc(m & ((1u << lane) - 1u));
-                if (f && slot < fq.cap) fq.idx[slot] = i + (uint64_t)j;
-            }
+    for (int d = 1; d < 32; d <<= 1) {
+        const unsigned t = __shfl_up_sync(act, incl, d);
+        if (lane >= (unsigned)d && ((act >> (lane - d)) & 1u)) incl += t;
+    }
+    const unsigned total = __shfl_sync(act, incl, 31 - __clz(act));
+    unsigned base = 0;
+    if ((int)lane == leader) base = atomicAdd(&bq.count, total);
+    base = __shfl_sync(act, base, leader);
+    unsigned slot = base + incl - c;
+    while (bits) {
+        const int j = __ffs(bits) - 1;
+        bits &= bits - 1u;
+        if (slot < fq.bcap) {
+            bq.idx[slot] = i + (uint64_t)j;
+        } else {  // block queue full: straight to the global queue
+            const unsigned long long g = atomicAdd(fq.count, 1ull);
+            if (g < fq.cap) fq.idx[g] = i + (uint64_t)j;
         }
+        ++slot;
+    }
+}
+
+// Publishes the block's queue (all threads of the block call it once).
+__device__ __forceinline__ void block_queue_flush(const FixQueue& fq, BlockQueue& bq) {
+    __syncthreads();
+    const unsigned cnt = min(bq.count, fq.bcap);
+    if (threadIdx.x == 0) bq.base = cnt ? atomicAdd(fq.count, (unsigned long long)cnt) : 0ull;
+    __syncthreads();
+    for (unsigned t = threadIdx.x; t < cnt; t += blockDim.x) {
+        const unsigned long long g = bq.base + t;
+        if (g < fq.cap) fq.idx[g] = bq.idx[t];
     }
 }
 
@@ -140,6 +181,8 @@ __global__ void __launch_bounds__(PhiloxLaunch<METHOD>::kBlock, PhiloxLaunch<MET
     philox_kernel(uint64_t first, int64_t n, float* __restrict__ hxp, float* __restrict__ hyp,
                   float* __restrict__ hzp, float* __restrict__ pdfp, FixQueue fq,
                   const __grid_constant__ PhiloxKeys ks) {
+    __shared__ BlockQueue bq;
+    if (METHOD == kCap) block_queue_init(bq);
     const int64_t nchunks = n / V;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -162,7 +205,7 @@ __global__ void __launch_bounds__(PhiloxLaunch<METHOD>::kBlock, PhiloxLaunch<MET
         st_stream<V>(hyp + i, hy);
         st_stream<V>(hzp + i, hz);
         if (PDF) st_stream<V>(pdfp + i, pd);
-        if (METHOD == kCap) queue_flags<V>(fq, flags, (uint64_t)i);
+        if (METHOD == kCap) queue_flags(fq, bq, flags, (uint64_t)i);
     }
     if (V > 1) {
         const int64_t i = nchunks * V + tid;
@@ -179,6 +222,7 @@ __global__ void __launch_bounds__(PhiloxLaunch<METHOD>::kBlock, PhiloxLaunch<MET
             }
         }
     }
+    if (METHOD == kCap) block_queue_flush(fq, bq);
 }
 
 // ------------------------------------------- fused Philox reflection (NEXT-2) --
@@ -202,6 +246,8 @@ template <int METHOD, int V, bool ALIGNED>
 __global__ void __launch_bounds__(PhiloxLaunch<METHOD>::kBlock, PhiloxLaunch<METHOD>::kMinBlocks)
     philox_reflect_kernel(uint64_t first, int64_t n, ReflectOut out, FixQueue fq,
                           const __grid_constant__ PhiloxKeys ks) {
+    __shared__ BlockQueue bq;
+    if (METHOD == kCap) block_queue_init(bq);
     const int64_t nchunks = n / V;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -226,7 +272,7 @@ __global__ void __launch_bounds__(PhiloxLaunch<METHOD>::kBlock, PhiloxLaunch<MET
         st_stream<V>(out.oz + i, oz);
         st_stream<V>(out.pdf + i, pd);
         st_stream<V>(out.weight + i, wg);
-        if (METHOD == kCap) queue_flags<V>(fq, flags, (uint64_t)i);
+        if (METHOD == kCap) queue_flags(fq, bq, flags, (uint64_t)i);
     }
     if (V > 1) {
         const int64_t i = nchunks * V + tid;
@@ -244,6 +290,7 @@ __global__ void __launch_bounds__(PhiloxLaunch<METHOD>::kBlock, PhiloxLaunch<MET
             }
         }
     }
+    if (METHOD == kCap) block_queue_flush(fq, bq);
 }
 
 __global__ void __launch_bounds__(128) philox_reflect_fixup_kernel(uint64_t seed, uint64_t first, int64_t n,

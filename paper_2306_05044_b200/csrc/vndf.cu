@@ -281,6 +281,18 @@ int64_t debug_fixup_cap() {
     return cap;
 }
 
+// Test hook: VNDF_DEBUG_BLOCK_QUEUE=k (read once) shrinks the fused kernels'
+// shared-memory block queues to k slots, so samples past them take the direct
+// global-queue path (tests/test_overflow_gpu.py).
+unsigned block_queue_cap() {
+    static const unsigned cap = [] {
+        const char* v = getenv("VNDF_DEBUG_BLOCK_QUEUE");
+        const long long k = v ? atoll(v) : 0;
+        return (unsigned)(k > 0 && k < kBlockQueue ? k : kBlockQueue);
+    }();
+    return cap;
+}
+
 StreamArgs make_args(const float* wx, const float* wy, const float* wz, const float* ax,
                      const float* ay, const float* u1, const float* u2, float* hx, float* hy,
                      float* hz, float* pdf) {
@@ -313,7 +325,7 @@ vndf_status launch_philox_v(uint64_t seed, uint64_t first, int64_t n, float* hx,
     int grid = 0;
     cudaError_t e = grid_for(k, block, std::max<int64_t>(n / V, 1), &grid, true);
     if (e != cudaSuccess) return cuda_fail(e);
-    FixQueue fq{nullptr, nullptr, 0};
+    FixQueue fq{nullptr, nullptr, 0, block_queue_cap()};
     void* qbuf = nullptr;
     if (METHOD == kCap) {
         // stream-ordered transient queue: [count | cap indices]
@@ -378,7 +390,7 @@ vndf_status launch_philox_reflect_v(uint64_t seed, uint64_t first, int64_t n, co
     int grid = 0;
     cudaError_t e = grid_for(k, block, std::max<int64_t>(n / V, 1), &grid, true);
     if (e != cudaSuccess) return cuda_fail(e);
-    FixQueue fq{nullptr, nullptr, 0};
+    FixQueue fq{nullptr, nullptr, 0, block_queue_cap()};
     void* qbuf = nullptr;
     if (METHOD == kCap) {
         fq.cap = (uint64_t)std::min<int64_t>(std::max<int64_t>(n / 128, 1 << 16), (int64_t)1 << 26);

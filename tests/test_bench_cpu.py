@@ -32,6 +32,11 @@ def test_issue_roofline(bench):
     assert r["achieved"] == pytest.approx(150.0 * r["warp_inst_per_sample"], rel=1e-3)
     assert r["frac"] == pytest.approx(r["achieved"] / r["peak"], rel=1e-3)
     assert r["gsamples_s_bound"] == pytest.approx(r["peak"] / r["warp_inst_per_sample"], rel=1e-3)
+    f = r["fma_pipe"]  # the FMA-datapath bound (measured per-instruction costs)
+    assert f["gsamples_s_bound"] == pytest.approx(148 * 4 * 1.965e9 * 32 / f["cycles_per_warp_sample"] / 1e9,
+                                                  rel=1e-3)
+    assert f["frac"] == pytest.approx(150.0 / f["gsamples_s_bound"], rel=1e-3)
+    assert f["gsamples_s_bound"] < r["gsamples_s_bound"]  # tighter than the issue bound
 
 
 def test_cpu_baseline_is_the_oracle(bench, orc):

@@ -1,8 +1,10 @@
-"""Fix-up queue overflow paths (vndf.cu test hook VNDF_DEBUG_FIXUP_CAP): with
-every queue shrunk to one entry, the streamed kernels fix the overflowing
-samples inline in the thread that found them and the fused kernels' fix-up
-kernel rescans every flag.  Results must be bit-identical to the normal path
-(which the parity tests hold against the oracle)."""
+"""Fix-up queue overflow paths (vndf.cu test hooks VNDF_DEBUG_FIXUP_CAP and
+VNDF_DEBUG_BLOCK_QUEUE): with every queue shrunk to one entry, the streamed
+kernels fix the overflowing samples inline in the thread that found them and
+the fused kernels' fix-up kernel rescans every flag; with only the fused
+kernels' shared-memory block queues shrunk, their overflowing samples go to the
+global queue directly.  Results must be bit-identical to the normal path (which
+the parity tests hold against the oracle)."""
 import os
 import subprocess
 import sys
@@ -42,12 +44,15 @@ def env():
     return True
 
 
-def _run(tmp_path, cap):
-    out = str(tmp_path / f"out_{cap}.npz")
+def _run(tmp_path, cap, block_cap=0):
+    out = str(tmp_path / f"out_{cap}_{block_cap}.npz")
     env = dict(os.environ)
     env.pop("VNDF_DEBUG_FIXUP_CAP", None)
+    env.pop("VNDF_DEBUG_BLOCK_QUEUE", None)
     if cap:
         env["VNDF_DEBUG_FIXUP_CAP"] = str(cap)
+    if block_cap:
+        env["VNDF_DEBUG_BLOCK_QUEUE"] = str(block_cap)
     code = _RUN.replace("ROOT", repr(ROOT)).replace("OUT", repr(out))
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
@@ -60,4 +65,11 @@ def test_overflow_paths_bit_identical(env, tmp_path):
     tiny = _run(tmp_path, 1)
     assert len(normal) == len(tiny) == 13
     for k, (a, b) in enumerate(zip(normal, tiny)):
+        np.testing.assert_array_equal(a, b, err_msg=f"output {k}")
+
+
+def test_block_queue_overflow_bit_identical(env, tmp_path):
+    normal = _run(tmp_path, 0)
+    small = _run(tmp_path, 0, block_cap=1)
+    for k, (a, b) in enumerate(zip(normal, small)):
         np.testing.assert_array_equal(a, b, err_msg=f"output {k}")
