@@ -28,7 +28,6 @@ struct StreamArgs {
     float* hy;
     float* hz;
     float* pdf;
-    int fix_cap;  // block fix-up queue slots used (<= kBlockFixCap; smaller only to test overflow)
 };
 
 // ---------------------------------------------------------------- memory ops
@@ -127,6 +126,15 @@ __device__ __forceinline__ bool sample_one(float wx, float wy, float wz, float a
     return false;
 }
 
-__device__ __forceinline__ void fix_one(const StreamArgs& a, bool pdf, int64_t i, bool flip) {
-    cap_fix_stream(a.wx, a.wy, a.wz, a.ax, a.ay, a.u1, a.u2, a.hx, a.hy, a.hz, pdf ? a.pdf : nullptr, i, flip);
+// Float64 recomputation of a flagged sample from its fp32 inputs (flip: the
+// flip frame of reading R4, else the native frame).
+__device__ __forceinline__ Sample fix_regs(float wx, float wy, float wz, float ax, float ay, float u1, float u2,
+                                           bool flip) {
+    const float4 f = cap_fp64(wx, wy, wz, ax, ay, u1, u2, flip);
+    Sample o;
+    o.x = f.x;
+    o.y = f.y;
+    o.z = f.z;
+    o.pdf = f.w;
+    return o;
 }

@@ -74,13 +74,13 @@ __global__ void __launch_bounds__(256) reflect_kernel(ReflectArgs a, int64_t n) 
                      ay = ld_stream<V>(a.ay + i), u1 = ld_stream<V>(a.u1 + i),
                      u2 = ld_stream<V>(a.u2 + i);
         Vec<V> ox, oy, oz, pd, wt;
-        unsigned flags = 0;
 #pragma unroll
         for (int j = 0; j < V; ++j) {
             Reflected r;
-            const bool f = cap_reflect_fp32(wx.v[j], wy.v[j], wz.v[j], ax.v[j], ay.v[j], u1.v[j] - 0.5f,
-                                            u2.v[j], 1.0f - u2.v[j], r);
-            flags |= (unsigned)f << j;
+            // a flagged sample is recomputed in float64 at once from its registers
+            if (cap_reflect_fp32(wx.v[j], wy.v[j], wz.v[j], ax.v[j], ay.v[j], u1.v[j] - 0.5f, u2.v[j],
+                                 1.0f - u2.v[j], r))
+                r = cap_reflect_fp64(wx.v[j], wy.v[j], wz.v[j], ax.v[j], ay.v[j], u1.v[j], u2.v[j]);
             ox.v[j] = r.x;
             oy.v[j] = r.y;
             oz.v[j] = r.z;
@@ -92,28 +92,20 @@ __global__ void __launch_bounds__(256) reflect_kernel(ReflectArgs a, int64_t n) 
         st_stream<V>(a.oz + i, oz);
         st_stream<V>(a.pdf + i, pd);
         st_stream<V>(a.weight + i, wt);
-        while (__builtin_expect(flags != 0, 0)) {
-            const int j = __ffs(flags) - 1;
-            flags &= flags - 1;
-            cap_reflect_fix_stream(a.wx, a.wy, a.wz, a.ax, a.ay, a.u1, a.u2, a.ox, a.oy, a.oz, a.pdf,
-                                   a.weight, i + j);
-        }
     }
     if (V > 1) {
         const int64_t i = nchunks * V + tid;
         if (i < n) {
+            const float wx = a.wx[i], wy = a.wy[i], wz = a.wz[i], ax = a.ax[i], ay = a.ay[i], u1 = a.u1[i],
+                        u2 = a.u2[i];
             Reflected r;
-            const float u2 = a.u2[i];
-            const bool f = cap_reflect_fp32(a.wx[i], a.wy[i], a.wz[i], a.ax[i], a.ay[i], a.u1[i] - 0.5f, u2,
-                                            1.0f - u2, r);
+            if (cap_reflect_fp32(wx, wy, wz, ax, ay, u1 - 0.5f, u2, 1.0f - u2, r))
+                r = cap_reflect_fp64(wx, wy, wz, ax, ay, u1, u2);
             a.ox[i] = r.x;
             a.oy[i] = r.y;
             a.oz[i] = r.z;
             a.pdf[i] = r.pdf;
             a.weight[i] = r.weight;
-            if (f)
-                cap_reflect_fix_stream(a.wx, a.wy, a.wz, a.ax, a.ay, a.u1, a.u2, a.ox, a.oy, a.oz, a.pdf,
-                                       a.weight, i);
         }
     }
 }

@@ -14,12 +14,13 @@
 #endif
 
 // ----------------------------------------------------- fused Philox kernel --
-// Deferred float64 fix-up queue of the fused kernel (compute-bound: inline
-// fp64 work would diverge the warp and its call would inflate the register
-// allocation).  Flagged local indices are appended with one atomicAdd per
-// flagged sample (~0.05% of the config-4 samples); a second kernel recomputes
-// them with all lanes busy.  If the queue overflowed (count > cap), the fix-up
-// kernel rescans every sample's flag instead: always correct, slower only then.
+// Deferred float64 fix-up of the fused kernel (compute-bound: an in-thread
+// float64 recomputation diverges the warp -- measured 138 against 147
+// Gsamples/s at config 4, profiles/r2/fused_variants_r2.txt).  Flagged local
+// indices (~0.05% of the config-4 samples) are queued per block (BlockQueue
+// below); a second kernel recomputes them with all lanes busy.  If the global
+// queue overflowed (count > cap), the fix-up kernel rescans every sample's
+// flag instead: always correct, slower only then.
 
 // Config-4 inputs of Philox counter ctr (both blocks, SURVEY s.8(d)).
 template <bool FW_HI>

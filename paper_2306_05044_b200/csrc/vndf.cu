@@ -246,10 +246,21 @@ int widest_vector(const StreamArgs& a) {
     return v;
 }
 
+// Small calls (fewer samples than one 8-sample chunk per thread of one
+// 128-thread block per SM) are latency-bound: 4-sample chunks in 64-thread
+// blocks spread them over more SMs and shorten each thread's chain (config 1,
+// 2^16 samples: cap 2.54 -> 1.95 us, Heitz 2.11 -> 1.62 us per launch;
+// profiles/r2/stream_fixup_r2.txt).  Explicit vndf_set_launch_config values win.
+bool small_call(int64_t n) {
+    int sms = 0;
+    if (sm_count(&sms) != cudaSuccess || sms <= 0) sms = 148;
+    return n < (int64_t)8 * 128 * sms;
+}
+
 template <int METHOD, bool PDF, int V>
 vndf_status launch_stream_v(const StreamArgs& a, int64_t n, cudaStream_t s) {
     const void* k = (const void*)stream_kernel<METHOD, PDF, V>;
-    const int block = block_size(128);
+    const int block = block_size(small_call(n) && prefs().block_size == 0 ? 64 : 128);
     int grid = 0;
     cudaError_t e = grid_for(k, block, std::max<int64_t>(n / V, 1), &grid, /*persistent=*/false);
     if (e != cudaSuccess) return cuda_fail(e);
@@ -261,17 +272,18 @@ vndf_status launch_stream_v(const StreamArgs& a, int64_t n, cudaStream_t s) {
 
 template <int METHOD, bool PDF>
 vndf_status launch_stream(const StreamArgs& a, int64_t n, cudaStream_t s) {
-    switch (widest_vector(a)) {
+    int v = widest_vector(a);
+    if (v == 8 && prefs().vector_width == 0 && small_call(n)) v = 4;
+    switch (v) {
         case 8: return launch_stream_v<METHOD, PDF, 8>(a, n, s);
         case 4: return launch_stream_v<METHOD, PDF, 4>(a, n, s);
         default: return launch_stream_v<METHOD, PDF, 1>(a, n, s);
     }
 }
 
-// Test hook: VNDF_DEBUG_FIXUP_CAP=k (read once) shrinks every fix-up queue
-// (block queues of the streamed kernels, global queues of the fused ones) to
-// k entries, so the overflow paths (inline fix-up / full rescan) run; results
-// are bit-identical by design (tests/test_overflow_gpu.py).
+// Test hook: VNDF_DEBUG_FIXUP_CAP=k (read once) shrinks the fused kernels'
+// global fix-up queues to k entries, so the overflow path (full rescan) runs;
+// results are bit-identical by design (tests/test_overflow_gpu.py).
 int64_t debug_fixup_cap() {
     static const int64_t cap = [] {
         const char* v = getenv("VNDF_DEBUG_FIXUP_CAP");
@@ -299,7 +311,6 @@ StreamArgs make_args(const float* wx, const float* wy, const float* wz, const fl
     StreamArgs a;
     a.wx = wx; a.wy = wy; a.wz = wz; a.ax = ax; a.ay = ay; a.u1 = u1; a.u2 = u2;
     a.hx = hx; a.hy = hy; a.hz = hz; a.pdf = pdf;
-    a.fix_cap = debug_fixup_cap() > 0 ? (int)std::min<int64_t>(debug_fixup_cap(), kBlockFixCap) : kBlockFixCap;
     return a;
 }
 

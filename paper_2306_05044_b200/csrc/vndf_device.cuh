@@ -292,18 +292,19 @@ __device__ __noinline__ float cap_reflect_weight_fp64(float wx, float wy, float 
     return (float)r[4];
 }
 
-__device__ __noinline__ void cap_reflect_fix_stream(const float* __restrict__ wx, const float* __restrict__ wy,
-                                                    const float* __restrict__ wz, const float* __restrict__ ax,
-                                                    const float* __restrict__ ay, const float* __restrict__ u1,
-                                                    const float* __restrict__ u2, float* ox, float* oy, float* oz,
-                                                    float* pdf, float* weight, int64_t i) {
+// Float64 recomputation of a flagged reflection sample from its fp32 inputs
+// (out of line: the streamed reflection kernel's vector loop keeps its registers).
+__device__ __noinline__ Reflected cap_reflect_fp64(float wx, float wy, float wz, float ax, float ay, float u1,
+                                                   float u2) {
     double r[5];
-    cap_reflect_fp64_d(wx[i], wy[i], wz[i], ax[i], ay[i], u1[i], u2[i], r);
-    ox[i] = (float)r[0];
-    oy[i] = (float)r[1];
-    oz[i] = (float)r[2];
-    pdf[i] = (float)r[3];
-    weight[i] = (float)r[4];
+    cap_reflect_fp64_d(wx, wy, wz, ax, ay, u1, u2, r);
+    Reflected o;
+    o.x = (float)r[0];
+    o.y = (float)r[1];
+    o.z = (float)r[2];
+    o.pdf = (float)r[3];
+    o.weight = (float)r[4];
+    return o;
 }
 
 // Out-of-line entry for the streamed kernels: widening happens in here, so the
@@ -311,22 +312,6 @@ __device__ __noinline__ void cap_reflect_fix_stream(const float* __restrict__ wx
 __device__ __noinline__ float4 cap_fp64(float wx, float wy, float wz, float ax, float ay, float u1,
                                         float u2, bool flip = true) {
     return cap_fp64_d(wx, wy, wz, ax, ay, u1, u2, flip);
-}
-
-// Streamed fix-up of sample i: re-reads its inputs (L2-resident: the chunk was
-// just loaded), recomputes in float64 and overwrites the fp32 outputs.  Called
-// after the chunk's vector stores, so the hot loop keeps no values live across
-// the call.
-__device__ __noinline__ void cap_fix_stream(const float* __restrict__ wx, const float* __restrict__ wy,
-                                            const float* __restrict__ wz, const float* __restrict__ ax,
-                                            const float* __restrict__ ay, const float* __restrict__ u1,
-                                            const float* __restrict__ u2, float* hx, float* hy,
-                                            float* hz, float* pdf, int64_t i, bool flip) {
-    const float4 f = cap_fp64_d(wx[i], wy[i], wz[i], ax[i], ay[i], u1[i], u2[i], flip);
-    hx[i] = f.x;
-    hy[i] = f.y;
-    hz[i] = f.z;
-    if (pdf) pdf[i] = f.w;
 }
 
 // ---------------------------------------------------------------------------
