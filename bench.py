@@ -519,6 +519,17 @@ def side_runs(torch, vndf, synth, dev, stream, c4_value):
     del o4
     torch.cuda.empty_cache()
 
+    # config 5's edge mix generated in-kernel (fused): grazing and below-horizon
+    # incidence in the compute-bound variant, cap vs Heitz on identical inputs
+    c5 = synth.CONFIGS[5]
+    o5 = vndf.empty_outputs(c5.n, dev)
+    t_ce = timed(lambda: vndf.vndf_sample_cap_philox_edge(c5.seed, 0, c5.n, *o5, stream=stream))
+    t_he = timed(lambda: vndf.vndf_sample_heitz2018_philox_edge(c5.seed, 0, c5.n, *o5, stream=stream))
+    res["c5_fused"] = {"gsamples_s": gs(c5.n, t_ce), "heitz_gsamples_s": gs(c5.n, t_he),
+                       "t_heitz_over_t_cap": round(t_he / t_ce, 4)}
+    del o5
+    torch.cuda.empty_cache()
+
     # config 3: 2^28 streamed, h only -- the HBM roofline run
     c3 = synth.CONFIGS[3]
     x3 = synth.fill(c3.recipe, c3.seed, c3.n, device=dev)

@@ -139,6 +139,28 @@ vndf_status vndf_sample_heitz2018_philox(uint64_t seed, uint64_t first_index, in
                                          float *h_x, float *h_y, float *h_z, float *pdf,
                                          vndf_stream_t stream);
 
+/* Fused in-kernel Philox4x32-10 on BASELINE config 5's path-tracer edge mix
+ * (north_star: the fused variant "evidenced by ... warp-divergence counters on
+ * grazing and below-horizon inputs").  Same counters and key as
+ * vndf_sample_cap_philox, u(w) = (w >> 8) 2^-24; the incidence category is
+ * v = u(Y2): v < 0.4 grazing z = 1e-4 + u(X0) (0.05 - 1e-4); v < 0.6 back
+ * side z = -(1 - u(X0)); else upper z = 1 - u(X0); phi = 2 pi u(X1),
+ * r = sqrt(max((1 - z)(1 + z), 0)); alpha_x = T[X2 >> 30], alpha_y = T[X3 >> 30],
+ * T = {1e-3, 0.05, 0.3, 1}; u1 = u(Y0), u2 = u(Y1), then Y3 bits 0-5 = 0 ->
+ * u1 = 0, bits 6-11 = 0 -> u2 = 0, bits 12-17 = 0 -> u2 = 1 - 2^-24 (a later
+ * rule wins).  These are, bit for bit, the fp32 inputs of the config-5
+ * recipe (DESIGN.md s.5); back-side incidence is flipped (reading R4) and the
+ * outputs equal vndf_sample_cap_pdf / vndf_sample_heitz2018 on those inputs.
+ * Outputs h and pdf (16 B per sample); pdf may be NULL. */
+vndf_status vndf_sample_cap_philox_edge(uint64_t seed, uint64_t first_index, int64_t n,
+                                        float *h_x, float *h_y, float *h_z, float *pdf,
+                                        vndf_stream_t stream);
+
+/* Heitz-2018 baseline on the same config-5 Philox inputs. pdf may be NULL. */
+vndf_status vndf_sample_heitz2018_philox_edge(uint64_t seed, uint64_t first_index, int64_t n,
+                                              float *h_x, float *h_y, float *h_z, float *pdf,
+                                              vndf_stream_t stream);
+
 /* Raw Philox4x32-10 words of block `block` for global indices
  * first_index .. first_index + n - 1: words[4k .. 4k+3] (test / audit).
  * words: device pointer to 4n uint32, 16-byte aligned (one uint4 per index). */

@@ -25,7 +25,8 @@ VNDF_ERR_NOT_IMPLEMENTED = 3
 # exported symbols of include/vndf.h (checked by tests/test_abi.py)
 SYMBOLS = (
     "vndf_sample_cap", "vndf_sample_cap_pdf", "vndf_sample_heitz2018",
-    "vndf_sample_cap_philox", "vndf_sample_heitz2018_philox", "vndf_philox4x32_10",
+    "vndf_sample_cap_philox", "vndf_sample_heitz2018_philox", "vndf_sample_cap_philox_edge",
+    "vndf_sample_heitz2018_philox_edge", "vndf_philox4x32_10",
     "vndf_sample_cap_pdf_host", "vndf_release_host_staging", "vndf_count_fixups", "vndf_count_fixups_philox",
     "vndf_set_launch_config", "vndf_status_string", "vndf_last_cuda_error", "vndf_version",
     "vndf_microbench", "vndf_sample_cap_reflect", "vndf_furnace", "vndf_pdf",
@@ -61,7 +62,8 @@ def lib() -> ctypes.CDLL:
         for name in ("vndf_sample_cap_pdf", "vndf_sample_heitz2018", "vndf_sample_cap_pdf_host",
                      "vndf_sample_cap_pdf_native"):
             getattr(L, name).argtypes = [P] * 11 + [i64, P]
-        for name in ("vndf_sample_cap_philox", "vndf_sample_heitz2018_philox"):
+        for name in ("vndf_sample_cap_philox", "vndf_sample_heitz2018_philox", "vndf_sample_cap_philox_edge",
+                     "vndf_sample_heitz2018_philox_edge"):
             getattr(L, name).argtypes = [u64, u64, i64, P, P, P, P, P]
         L.vndf_philox4x32_10.argtypes = [u64, u64, i64, u32, P, P]
         L.vndf_count_fixups.argtypes = [P] * 7 + [i64, P, P]
@@ -229,6 +231,15 @@ def vndf_sample_cap_philox(seed, first_index, n, h_x, h_y, h_z, pdf=None, stream
 
 def vndf_sample_heitz2018_philox(seed, first_index, n, h_x, h_y, h_z, pdf=None, stream=None):
     _philox_call("vndf_sample_heitz2018_philox", seed, first_index, n, h_x, h_y, h_z, pdf, stream)
+
+
+def vndf_sample_cap_philox_edge(seed, first_index, n, h_x, h_y, h_z, pdf=None, stream=None):
+    """Fused Philox4x32-10 inputs of the config-5 edge mix + spherical-cap sampling + pdf."""
+    _philox_call("vndf_sample_cap_philox_edge", seed, first_index, n, h_x, h_y, h_z, pdf, stream)
+
+
+def vndf_sample_heitz2018_philox_edge(seed, first_index, n, h_x, h_y, h_z, pdf=None, stream=None):
+    _philox_call("vndf_sample_heitz2018_philox_edge", seed, first_index, n, h_x, h_y, h_z, pdf, stream)
 
 
 def vndf_philox4x32_10(seed, first_index, n, block, words, stream=None):

@@ -34,6 +34,28 @@ __device__ __forceinline__ Inputs c4_inputs_seed(uint64_t seed, uint64_t ctr) {
     return c4_inputs_fp32(philox_block(seed, ctr, 0u), philox_block(seed, ctr, 1u));
 }
 
+// In-kernel input recipes of the fused sample kernels: kRecipeC4 = BASELINE
+// config 4 (upper hemisphere, log-uniform alpha), kRecipeC5 = config 5 (edge
+// mix: grazing, below-horizon and upper incidence, alpha from a 4-value set,
+// u = 0 and rim injections).
+constexpr int kRecipeC4 = 4, kRecipeC5 = 5;
+
+template <int RECIPE>
+__device__ __forceinline__ Inputs recipe_inputs_seed(uint64_t seed, uint64_t ctr) {
+    const uint4 X = philox_block(seed, ctr, 0u), Y = philox_block(seed, ctr, 1u);
+    return RECIPE == kRecipeC5 ? c5_inputs_fp32(X, Y) : c4_inputs_fp32(X, Y);
+}
+
+// Float64 recomputation of a flagged fused sample: config 4 from the exact
+// uniforms (c4_inputs_fp64), config 5 from its fp32 inputs (the streamed
+// kernels' fix-up of the same inputs).
+template <int RECIPE>
+__device__ __forceinline__ float4 recipe_cap_fp64(uint64_t seed, uint64_t ctr) {
+    if (RECIPE == kRecipeC4) return cap_philox_fp64(seed, ctr);
+    const Inputs in = recipe_inputs_seed<RECIPE>(seed, ctr);
+    return cap_fp64(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1 + 0.5f, in.u2, true);
+}
+
 // Block-level fix-up queue of the fused kernels.  Flagged local indices are
 // collected in shared memory (a warp reserves its slots with one shared-memory
 // atomic) and published to the global queue once per block at the end of the
@@ -105,8 +127,17 @@ __device__ __forceinline__ void block_queue_flush(const FixQueue& fq, BlockQueue
 
 // ctr = first + k, the Philox counter of local sample k; returns the
 // conditioning flag (always false for Heitz)
-template <int METHOD, bool PDF>
+template <int METHOD, bool PDF, int RECIPE = kRecipeC4>
 __device__ __forceinline__ bool philox_one(const PhiloxKeys& ks, uint64_t ctr, Sample& o) {
+    if (RECIPE == kRecipeC5) {
+        // edge mix: back-side incidence is flipped (reading R4), as in the streamed kernels
+        uint4 X, Y;
+        philox_pair_ks(ks, ctr, X, Y);
+        const Inputs in = c5_inputs_fp32(X, Y);
+        if (METHOD == kCap) return cap_fp32<PDF>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o);
+        heitz_fp32<PDF>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, o);
+        return false;
+    }
     const Inputs in = c4_inputs_ks<VNDF_CAP_FW_HI && METHOD == kCap>(ks, ctr);
     if (METHOD == kCap) {
         // config-4 inputs are on the upper hemisphere (wi.z = 1 - u > 0): no flip
@@ -116,6 +147,7 @@ __device__ __forceinline__ bool philox_one(const PhiloxKeys& ks, uint64_t ctr, S
     return false;
 }
 
+template <int RECIPE>
 __global__ void __launch_bounds__(128) philox_fixup_kernel(uint64_t seed, uint64_t first, int64_t n,
                                                             FixQueue fq, float* __restrict__ hx,
                                                             float* __restrict__ hy, float* __restrict__ hz,
@@ -123,27 +155,24 @@ __global__ void __launch_bounds__(128) philox_fixup_kernel(uint64_t seed, uint64
     const uint64_t count = *fq.count;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    auto fix = [&](uint64_t k) {
+        const float4 f = recipe_cap_fp64<RECIPE>(seed, first + k);
+        hx[k] = f.x;
+        hy[k] = f.y;
+        hz[k] = f.z;
+        if (pdf) pdf[k] = f.w;
+    };
     if (count <= fq.cap) {
-        for (uint64_t t = t0; t < count; t += stride) {
-            const uint64_t k = fq.idx[t];
-            const float4 f = cap_philox_fp64(seed, first + k);
-            hx[k] = f.x;
-            hy[k] = f.y;
-            hz[k] = f.z;
-            if (pdf) pdf[k] = f.w;
-        }
+        for (uint64_t t = t0; t < count; t += stride) fix(fq.idx[t]);
         return;
     }
     for (uint64_t k = t0; k < (uint64_t)n; k += stride) {  // overflow: rescan
-        const Inputs in = c4_inputs_seed(seed, first + k);
+        const Inputs in = recipe_inputs_seed<RECIPE>(seed, first + k);
         Sample o;
-        if (cap_fp32<true, kFrameUpper>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o)) {
-            const float4 f = cap_philox_fp64(seed, first + k);
-            hx[k] = f.x;
-            hy[k] = f.y;
-            hz[k] = f.z;
-            if (pdf) pdf[k] = f.w;
-        }
+        const bool f = RECIPE == kRecipeC5
+                           ? cap_fp32<true>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o)
+                           : cap_fp32<true, kFrameUpper>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o);
+        if (f) fix(k);
     }
 }
 
@@ -177,7 +206,7 @@ struct PhiloxLaunch {
 
 // ALIGNED: first is a multiple of V, so the counters of a chunk share their
 // high word and differ only in the low bits (no 64-bit add per sample).
-template <int METHOD, bool PDF, int V, bool ALIGNED>
+template <int METHOD, bool PDF, int V, bool ALIGNED, int RECIPE = kRecipeC4>
 __global__ void __launch_bounds__(PhiloxLaunch<METHOD>::kBlock, PhiloxLaunch<METHOD>::kMinBlocks)
     philox_kernel(uint64_t first, int64_t n, float* __restrict__ hxp, float* __restrict__ hyp,
                   float* __restrict__ hzp, float* __restrict__ pdfp, FixQueue fq,
@@ -196,7 +225,7 @@ __global__ void __launch_bounds__(PhiloxLaunch<METHOD>::kBlock, PhiloxLaunch<MET
         for (int j = 0; j < V; ++j) {
             const uint64_t ctr = ALIGNED ? (base | (uint64_t)j) : base + (uint64_t)j;
             Sample o;
-            flags |= (unsigned)philox_one<METHOD, PDF>(ks, ctr, o) << j;
+            flags |= (unsigned)philox_one<METHOD, PDF, RECIPE>(ks, ctr, o) << j;
             hx.v[j] = o.x;
             hy.v[j] = o.y;
             hz.v[j] = o.z;
@@ -212,7 +241,7 @@ __global__ void __launch_bounds__(PhiloxLaunch<METHOD>::kBlock, PhiloxLaunch<MET
         const int64_t i = nchunks * V + tid;
         if (i < n) {
             Sample o;
-            const bool f = philox_one<METHOD, PDF>(ks, first + (uint64_t)i, o);
+            const bool f = philox_one<METHOD, PDF, RECIPE>(ks, first + (uint64_t)i, o);
             hxp[i] = o.x;
             hyp[i] = o.y;
             hzp[i] = o.z;

@@ -11,8 +11,9 @@
 //   kernels_stream.cuh   stream_kernel<METHOD, PDF, V>: streamed SoA sampling
 //                        (cap, Heitz, native cap), one V-sample chunk per
 //                        thread, block-level float64 fix-up queue
-//   kernels_philox.cuh   philox_kernel<METHOD, PDF, V, ALIGNED>: fused
-//                        Philox4x32-10 generation + sampling + pdf;
+//   kernels_philox.cuh   philox_kernel<METHOD, PDF, V, ALIGNED, RECIPE>: fused
+//                        Philox4x32-10 generation (config-4 or config-5
+//                        recipe) + sampling + pdf;
 //                        philox_reflect_kernel: the same + reflection, Eq. 20
 //                        pdf and G2/G1 weight (NEXT-2); deferred fix-up queues
 //                        and kernels; raw Philox words; fix-up counters
@@ -328,10 +329,10 @@ vndf_status validate_philox_out(int64_t n, float* hx, float* hy, float* hz, floa
     return VNDF_OK;
 }
 
-template <int METHOD, bool PDF, int V, bool ALIGNED>
+template <int METHOD, bool PDF, int V, bool ALIGNED, int RECIPE>
 vndf_status launch_philox_v(uint64_t seed, uint64_t first, int64_t n, float* hx, float* hy, float* hz,
                             float* pdf, cudaStream_t s) {
-    const void* k = (const void*)philox_kernel<METHOD, PDF, V, ALIGNED>;
+    const void* k = (const void*)philox_kernel<METHOD, PDF, V, ALIGNED, RECIPE>;
     const int block = block_size(PhiloxLaunch<METHOD>::kBlock);
     int grid = 0;
     cudaError_t e = grid_for(k, block, std::max<int64_t>(n / V, 1), &grid, true);
@@ -352,7 +353,8 @@ vndf_status launch_philox_v(uint64_t seed, uint64_t first, int64_t n, float* hx,
             return cuda_fail(e);
         }
     }
-    philox_kernel<METHOD, PDF, V, ALIGNED><<<grid, block, 0, s>>>(first, n, hx, hy, hz, pdf, fq, philox_keys(seed));
+    philox_kernel<METHOD, PDF, V, ALIGNED, RECIPE>
+        <<<grid, block, 0, s>>>(first, n, hx, hy, hz, pdf, fq, philox_keys(seed));
     e = cudaGetLastError();
     if (e == cudaSuccess && METHOD == kCap) {
         // one thread per queue slot up to SMs x 32 blocks; blocks past the
@@ -361,7 +363,7 @@ vndf_status launch_philox_v(uint64_t seed, uint64_t first, int64_t n, float* hx,
         e = sm_count(&sms);
         const int64_t fix_blocks = std::min<int64_t>(((int64_t)fq.cap + 127) / 128, (int64_t)std::max(sms, 1) * 32);
         if (e == cudaSuccess) {
-            philox_fixup_kernel<<<(int)fix_blocks, 128, 0, s>>>(seed, first, n, fq, hx, hy, hz, pdf);
+            philox_fixup_kernel<RECIPE><<<(int)fix_blocks, 128, 0, s>>>(seed, first, n, fq, hx, hy, hz, pdf);
             e = cudaGetLastError();
         }
     }
@@ -372,7 +374,7 @@ vndf_status launch_philox_v(uint64_t seed, uint64_t first, int64_t n, float* hx,
     return e == cudaSuccess ? VNDF_OK : cuda_fail(e);
 }
 
-template <int METHOD>
+template <int METHOD, int RECIPE = kRecipeC4>
 vndf_status launch_philox(uint64_t seed, uint64_t first, int64_t n, float* hx, float* hy, float* hz,
                           float* pdf, cudaStream_t s) {
     vndf_status st = validate_philox_out(n, hx, hy, hz, pdf);
@@ -382,13 +384,13 @@ vndf_status launch_philox(uint64_t seed, uint64_t first, int64_t n, float* hx, f
     if (prefs().vector_width == 1) v4 = false;
     const bool al = first % PV == 0;  // counters of a chunk share their high word
     if (pdf) {
-        if (!v4) return launch_philox_v<METHOD, true, 1, true>(seed, first, n, hx, hy, hz, pdf, s);
-        return al ? launch_philox_v<METHOD, true, PV, true>(seed, first, n, hx, hy, hz, pdf, s)
-                  : launch_philox_v<METHOD, true, PV, false>(seed, first, n, hx, hy, hz, pdf, s);
+        if (!v4) return launch_philox_v<METHOD, true, 1, true, RECIPE>(seed, first, n, hx, hy, hz, pdf, s);
+        return al ? launch_philox_v<METHOD, true, PV, true, RECIPE>(seed, first, n, hx, hy, hz, pdf, s)
+                  : launch_philox_v<METHOD, true, PV, false, RECIPE>(seed, first, n, hx, hy, hz, pdf, s);
     }
-    if (!v4) return launch_philox_v<METHOD, false, 1, true>(seed, first, n, hx, hy, hz, pdf, s);
-    return al ? launch_philox_v<METHOD, false, PV, true>(seed, first, n, hx, hy, hz, pdf, s)
-              : launch_philox_v<METHOD, false, PV, false>(seed, first, n, hx, hy, hz, pdf, s);
+    if (!v4) return launch_philox_v<METHOD, false, 1, true, RECIPE>(seed, first, n, hx, hy, hz, pdf, s);
+    return al ? launch_philox_v<METHOD, false, PV, true, RECIPE>(seed, first, n, hx, hy, hz, pdf, s)
+              : launch_philox_v<METHOD, false, PV, false, RECIPE>(seed, first, n, hx, hy, hz, pdf, s);
 }
 
 // Fused Philox reflection (NEXT-2): same grid, table, queue and fix-up
@@ -634,6 +636,18 @@ vndf_status vndf_sample_heitz2018_philox(uint64_t seed, uint64_t first_index, in
                                          float* h_y, float* h_z, float* pdf, vndf_stream_t stream) {
     DeviceGuard device_guard((cudaStream_t)stream);
     return launch_philox<kHeitz>(seed, first_index, n, h_x, h_y, h_z, pdf, (cudaStream_t)stream);
+}
+
+vndf_status vndf_sample_cap_philox_edge(uint64_t seed, uint64_t first_index, int64_t n, float* h_x,
+                                        float* h_y, float* h_z, float* pdf, vndf_stream_t stream) {
+    DeviceGuard device_guard((cudaStream_t)stream);
+    return launch_philox<kCap, kRecipeC5>(seed, first_index, n, h_x, h_y, h_z, pdf, (cudaStream_t)stream);
+}
+
+vndf_status vndf_sample_heitz2018_philox_edge(uint64_t seed, uint64_t first_index, int64_t n, float* h_x,
+                                              float* h_y, float* h_z, float* pdf, vndf_stream_t stream) {
+    DeviceGuard device_guard((cudaStream_t)stream);
+    return launch_philox<kHeitz, kRecipeC5>(seed, first_index, n, h_x, h_y, h_z, pdf, (cudaStream_t)stream);
 }
 
 vndf_status vndf_philox4x32_10(uint64_t seed, uint64_t first_index, int64_t n, uint32_t block,

@@ -606,6 +606,48 @@ __device__ __forceinline__ Inputs c4_inputs_fp32(uint4 X, uint4 Y) {
     return in;
 }
 
+// Config-5 inputs (BASELINE config 5, path-tracer edge mix; DESIGN.md s.5
+// recipe 5) from the two words blocks of a sample, in the recipe's fp32
+// operations, so the fused edge kernels sample exactly the fp32 inputs that
+// the streamed kernels read from planes generated by the same recipe:
+//   category v = u(Y2): v < 0.4 grazing z = 1e-4 + u(X0) (0.05 - 1e-4),
+//   v < 0.6 back side z = -(1 - u(X0)), else upper z = 1 - u(X0);
+//   phi = 2 pi u(X1), r = sqrt(max((1 - z)(1 + z), 0));
+//   alpha_x = T[X2 >> 30], alpha_y = T[X3 >> 30], T = {1e-3, 0.05, 0.3, 1};
+//   u1 = u(Y0), u2 = u(Y1); Y3 bits 0-5 = 0 -> u1 = 0, bits 6-11 = 0 -> u2 = 0,
+//   bits 12-17 = 0 -> u2 = 1 - 2^-24 (the rim; a later rule wins).
+__device__ __forceinline__ float alpha_edge(uint32_t w) {
+    // two selects on the index bits (a compare chain compiled to divergent branches)
+    const bool b0 = (w >> 30) & 1u, b1 = (w >> 31) != 0u;
+    const float lo = b0 ? 0.05f : 1e-3f, hi = b0 ? 1.0f : 0.3f;
+    return b1 ? hi : lo;
+}
+
+__device__ __forceinline__ Inputs c5_inputs_fp32(uint4 X, uint4 Y) {
+    const float ua = __uint2float_rn(X.x >> 8) * 0x1p-24f;
+    float sp, cp;
+    sincospif(2.0f * (__uint2float_rn(X.y >> 8) * 0x1p-24f), &sp, &cp);
+    const float v = __uint2float_rn(Y.z >> 8) * 0x1p-24f;
+    // branch-free: all three categories, then selects
+    const float z_graze = 1e-4f + ua * (0.05f - 1e-4f), z_upper = 1.0f - ua;
+    const float z = v < 0.4f ? z_graze : v < 0.6f ? -z_upper : z_upper;
+    const float r = sqrtf(fmaxf((1.0f - z) * (1.0f + z), 0.0f));
+    float u1 = __uint2float_rn(Y.x >> 8) * 0x1p-24f, u2 = __uint2float_rn(Y.y >> 8) * 0x1p-24f;
+    if ((Y.w & 0x3Fu) == 0u) u1 = 0.0f;
+    if (((Y.w >> 6) & 0x3Fu) == 0u) u2 = 0.0f;
+    if (((Y.w >> 12) & 0x3Fu) == 0u) u2 = 1.0f - 0x1p-24f;
+    Inputs in;
+    in.wx = r * cp;
+    in.wy = r * sp;
+    in.wz = z;
+    in.ax = alpha_edge(X.z);
+    in.ay = alpha_edge(X.w);
+    in.v1 = u1 - 0.5f;  // exact: u1 is on the 2^-24 grid
+    in.u2 = u2;
+    in.q = 1.0f - u2;
+    return in;
+}
+
 __device__ __forceinline__ double u01d(uint32_t w) { return (double)(w >> 8) * 0x1p-24; }
 
 // The config-4 inputs of a sample in double from the exact uniforms:

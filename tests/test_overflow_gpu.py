@@ -1,10 +1,10 @@
-"""Fix-up queue overflow paths (vndf.cu test hooks VNDF_DEBUG_FIXUP_CAP and
-VNDF_DEBUG_BLOCK_QUEUE): with every queue shrunk to one entry, the streamed
-kernels fix the overflowing samples inline in the thread that found them and
-the fused kernels' fix-up kernel rescans every flag; with only the fused
-kernels' shared-memory block queues shrunk, their overflowing samples go to the
-global queue directly.  Results must be bit-identical to the normal path (which
-the parity tests hold against the oracle)."""
+"""Fix-up queue overflow paths of the fused kernels (vndf.cu test hooks
+VNDF_DEBUG_FIXUP_CAP and VNDF_DEBUG_BLOCK_QUEUE): with the global queue shrunk
+to one entry the fix-up kernel rescans every flag; with only the shared-memory
+block queues shrunk, the overflowing samples go to the global queue directly.
+Results must be bit-identical to the normal path (which the parity tests hold
+against the oracle).  The streamed kernels (fix-ups in the flagged thread, no
+queue) are run too, as a control."""
 import os
 import subprocess
 import sys
@@ -30,8 +30,10 @@ p = vndf.empty_outputs(n, dev)
 vndf.vndf_sample_cap_philox(3, 5, n, *p)
 r = [torch.empty(n, device=dev) for _ in range(5)]
 vndf.vndf_sample_cap_reflect_philox(3, 5, n, *r)
+e = vndf.empty_outputs(n, dev)
+vndf.vndf_sample_cap_philox_edge(4, 5, n, *e)
 torch.cuda.synchronize()
-np.savez(OUT, *[t.cpu().numpy() for t in list(o) + list(p) + r])
+np.savez(OUT, *[t.cpu().numpy() for t in list(o) + list(p) + r + list(e)])
 """
 
 
@@ -63,7 +65,7 @@ def _run(tmp_path, cap, block_cap=0):
 def test_overflow_paths_bit_identical(env, tmp_path):
     normal = _run(tmp_path, 0)
     tiny = _run(tmp_path, 1)
-    assert len(normal) == len(tiny) == 13
+    assert len(normal) == len(tiny) == 17
     for k, (a, b) in enumerate(zip(normal, tiny)):
         np.testing.assert_array_equal(a, b, err_msg=f"output {k}")
 

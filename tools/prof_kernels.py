@@ -1,6 +1,6 @@
 """Small driver for ncu captures: a few launches of each hot kernel.
 
-python tools/prof_kernels.py [which]   which in {all, c2, c3, c4, c5}
+python tools/prof_kernels.py [which]   which in {all, c2, c3, c4, c5, c5fused, reflect_philox, next}
 """
 import os
 import sys
@@ -37,6 +37,13 @@ if which in ("all", "c4"):
     for _ in range(2):
         vndf.vndf_sample_cap_philox(3, 0, n, *o)
         vndf.vndf_sample_heitz2018_philox(3, 0, n, *o)
+    torch.cuda.synchronize()
+if which in ("all", "c5fused"):
+    n = 1 << 26
+    o = vndf.empty_outputs(n, dev)
+    for _ in range(2):
+        vndf.vndf_sample_cap_philox_edge(4, 0, n, *o)
+        vndf.vndf_sample_heitz2018_philox_edge(4, 0, n, *o)
     torch.cuda.synchronize()
 if which in ("all", "reflect_philox"):
     n = 1 << 26
