@@ -254,8 +254,7 @@ def issue_roofline(gsamples_s: float, key: str, n_per_launch: int = None, launch
     out = {"bound": "alu", "achieved": round(achieved, 2), "peak": round(peak, 2), "unit": "Gwarp-inst/s",
            "frac": round(achieved / peak, 4), "traffic": None,
            "warp_inst_per_sample": inst, "gsamples_s_bound": round(peak / inst, 2),
-           "model": f"{SMS} SMs x {SMSPS_PER_SM} SMSPs x 1 warp-inst/clk x {SM_MAX_MHZ:.0f} MHz; "
-                    f"{inst} warp-inst/sample (ncu sm__inst_executed / samples)"}
+           "model": "592 SMSPs x 1 warp-inst/clk x 1965 MHz; ncu warp-inst/sample (DESIGN.md s.6.4)"}
     # the FMA datapath: IMAD.WIDE.U32 (Philox) holds it ~4.3 clk per warp-instruction
     # and does not overlap with FP32 FFMA/FMUL on B200 (tools/mix_probe.cu), so the
     # sum of the measured per-instruction costs bounds the kernel (DESIGN.md s.6.4)
@@ -264,8 +263,7 @@ def issue_roofline(gsamples_s: float, key: str, n_per_launch: int = None, launch
         bound = SMS * SMSPS_PER_SM * f * 32 / cyc / 1e9
         out["fma_pipe"] = {"cycles_per_warp_sample": cyc, "gsamples_s_bound": round(bound, 2),
                            "frac": round(gsamples_s / bound, 4),
-                           "model": "IMAD.WIDE 4.335 clk + FP32 FMA-pipe instruction 1.03 clk + IMAD 2 clk "
-                                    "per warp-instruction (measured), ncu dynamic counts per sample"}
+                           "model": "measured clk per IMAD.WIDE / FP32 / IMAD x ncu counts (DESIGN.md s.6.4)"}
     return out
 
 
@@ -316,8 +314,7 @@ def cpu_baseline(check=None, c1_planes=None, c3_planes=None, budget_s: float = 1
             break
     dt = time.perf_counter() - t0
     out = {"value": round(done / dt / 1e9, 5), "unit": UNIT, "cores": T, "kind": "oracle",
-           "sample": f"config 4 recipe (float64 Philox inputs + Listing 1+3 + Eq. 1 pdf), indices [0, 2^22), "
-                     f"{done // m} passes of {m} in {dt:.1f} s on {T} threads",
+           "sample": f"config-4 indices [0, 2^22) x {done // m} in {dt:.1f} s, {T} threads",
            "cpu_model": _cpu_model()}
     sub = {}
     ns, n1 = 1 << log2_sub, 1 << (log2_sub - 4)
@@ -325,21 +322,21 @@ def cpu_baseline(check=None, c1_planes=None, c3_planes=None, budget_s: float = 1
     r1, k1 = _rate(lambda: oracle.batch_sample_philox(oracle.CAP, C4_SEED, i24[:n1], threads=1), n1, 5)
     rT, kT = _rate(lambda: oracle.batch_sample_philox(oracle.CAP, C4_SEED, i24, threads=T), ns, 5)
     sub["c4_2e24"] = {"T_threads": round(rT, 5), "1_thread": round(r1, 5), "runs": [kT, k1],
-                      "note": "T threads: median of 5 on [0, 2^24); 1 thread: median of 5 on [0, 2^20)"}
+                      "note": "T: median of 5 on 2^24; 1: on 2^20"}
     if c1_planes is not None:
         n1p = c1_planes[0].size
         rT, kT = _rate(lambda: oracle.batch_sample(oracle.CAP, *c1_planes, pdf=True, threads=T), n1p, 100)
         r1, k1 = _rate(lambda: oracle.batch_sample(oracle.CAP, *c1_planes, pdf=True, threads=1), n1p, 100,
                        budget_s=2.0)
         sub["c1_2e16"] = {"T_threads": round(rT, 5), "1_thread": round(r1, 5), "runs": [kT, k1],
-                          "note": "median of 100 runs (1 thread: of as many as fit in 2 s)"}
+                          "note": "median of 100 (1 thread: within 2 s)"}
     if c3_planes is not None:
         rT, kT = _rate(lambda: oracle.batch_sample(oracle.CAP, *c3_planes, pdf=False, threads=T),
                        c3_planes[0].size, 5)
         one = [p[:n1] for p in c3_planes]
         r1, k1 = _rate(lambda: oracle.batch_sample(oracle.CAP, *one, pdf=False, threads=1), one[0].size, 5)
         sub["c3_2e24"] = {"T_threads": round(rT, 5), "1_thread": round(r1, 5), "runs": [kT, k1],
-                          "note": "T threads: median of 5 on the first 2^24 config-3 samples; 1 thread: 2^20"}
+                          "note": "T: median of 5 on 2^24; 1: on 2^20"}
     out["subranges"] = sub
     if check is not None:
         ci, ch, cp = check
@@ -435,7 +432,7 @@ def run_ours(args):
         rl["traffic"] = _profiled("cap_philox_c4_dram_bytes")
         rl["algorithmic_bytes_per_launch"] = 16 * n
         rl["pipes_ncu"] = _profiled("cap_philox_c4_pipes")
-        rl["kernel"] = "philox_kernel<cap, pdf, 8> (+ philox_fixup_kernel; timed as the whole step)"
+        rl["kernel"] = "philox_kernel<cap> + philox_fixup_kernel (the whole step)"
 
     # ---- end to end: the host-buffer entry point, pinned host outputs ----
     e2e = None
@@ -451,22 +448,34 @@ def run_ours(args):
             vndf.vndf_sample_cap_philox_host(C4_SEED, first, n, *hout)
         e2e_s = reduce_max(time.perf_counter() - t0, world, dev)
         same = bool(hashlib.sha256(b"".join(t[: 1 << 24].numpy().tobytes() for t in hout)).hexdigest() == out_sha)
+        # the host link's own device -> pinned host rate (a plain 1 GiB copy): the e2e ceiling
+        src = torch.empty(1 << 28, dtype=torch.float32, device=dev)
+        dst = torch.empty(1 << 28, dtype=torch.float32, pin_memory=True)
+        dst.copy_(src)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        for _ in range(3):
+            dst.copy_(src)
+        torch.cuda.synchronize()
+        link_peak = 3 * (1 << 30) / (time.perf_counter() - t1) / 1e9
+        del src, dst
+        link = 16 * n * e2e_steps / e2e_s / 1e9
         e2e = {"value": round(world * n * e2e_steps / e2e_s / 1e9, 4), "unit": UNIT,
                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 16 * n,
-               "api": "vndf_sample_cap_philox_host (blocking; pinned host outputs written by the kernel "
-                      "across the host link; inputs are seed + index range, nothing host -> device)",
+               "api": "vndf_sample_cap_philox_host (pinned host outputs written across the link)",
                "steps": e2e_steps, "bit_identical_to_device": same,
-               "link_gb_s": round(16 * n * e2e_steps / e2e_s / 1e9, 2)}
+               "link_gb_s": round(link, 2), "link_d2h_copy_gb_s": round(link_peak, 2),
+               "frac_of_link": round(link / link_peak, 4)}
         del hout
 
     result = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (in-kernel Philox4x32-10, SURVEY 8(d) config-4 recipe)",
+        "data": "synthetic (in-kernel Philox4x32-10, config-4 recipe)",
         "config": {"workload": f"config 4: {cfg.label}", "samples_per_gpu_per_step": n,
                    "kernel": "vndf_sample_cap_philox", "parallelism": f"independent shards x{world}",
-                   "l2": "17.2 GB written per step >> 126 MB L2; no flush"},
+                   "l2": "17.2 GB written per step >> 126 MB L2, no flush"},
         "roofline": rl,
         "clocks": clocks.summary(),
         "e2e": e2e,
@@ -491,9 +500,41 @@ def run_ours(args):
     elif rank == 0:
         result["cpu_baseline"] = None
     if rank == 0:
-        print(json.dumps(result, separators=(",", ":")), flush=True)
+        print(json.dumps(ordered(result), separators=(",", ":")), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+CONTRACT_KEYS = ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                 "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "clocks", "e2e", "gpu_launches")
+
+
+def summary(r):
+    """The per-config headline numbers in one short object, placed right after
+    the contract keys (a record that keeps only the head of the line keeps them)."""
+    def g(*path):
+        v = r
+        for k in path:
+            if not isinstance(v, dict) or k not in v:
+                return None
+            v = v[k]
+        return v
+    return {"c4_gsamples_s": r.get("value"), "c4_frac_issue": g("roofline", "frac"),
+            "c4_frac_fma_pipe": g("roofline", "fma_pipe", "frac"), "c4_t_heitz_over_t_cap": g("heitz_c4", "t_heitz_over_t_cap"),
+            "c3_gb_s": g("c3", "gb_s"), "c3_frac_hbm": g("c3", "frac_hbm"), "c3_t_heitz_over_t_cap": g("c3", "t_heitz_over_t_cap"),
+            "c5_t_heitz_over_t_cap": g("c5", "t_heitz_over_t_cap"),
+            "c5_fused_t_heitz_over_t_cap": g("c5_fused", "t_heitz_over_t_cap"),
+            "c1_cap_us": g("c1", "cap_us"), "c1_t_heitz_over_t_cap": g("c1", "t_heitz_over_t_cap"),
+            "c2_frac_hbm": g("c2", "frac_hbm"),
+            "sampler_only_t_heitz_over_t_cap": g("next", "microbench_t_heitz_over_t_cap"),
+            "parity_over_tol": g("parity", "over_tol"), "cpu_oracle_gsamples_s": g("cpu_baseline", "value")}
+
+
+def ordered(r):
+    out = {k: r[k] for k in CONTRACT_KEYS if k in r}
+    out["summary"] = summary(r)
+    out.update({k: v for k, v in r.items() if k not in out})
+    return out
 
 
 def side_runs(torch, vndf, synth, dev, stream, c4_value):
@@ -539,7 +580,8 @@ def side_runs(torch, vndf, synth, dev, stream, c4_value):
     t_hz3 = timed(lambda: vndf.vndf_sample_heitz2018(*ins3, *o3, None, stream=stream))
     rl3 = roofline(40 * c3.n, t_cap3, "cap_c3")
     res["c3"] = {"gsamples_s": gs(c3.n, t_cap3), "ms": round(t_cap3, 4), "gb_s": rl3["achieved"],
-                 "frac_hbm": rl3["frac"], "t_heitz_over_t_cap": round(t_hz3 / t_cap3, 4), "roofline": rl3}
+                 "frac_hbm": rl3["frac"], "t_heitz_over_t_cap": round(t_hz3 / t_cap3, 4), "roofline": rl3,
+                 "inputs_sha256_first_2e20": _sha256(ins3, 1 << 20)[:16]}
     del x3, o3, ins3
     torch.cuda.empty_cache()
 

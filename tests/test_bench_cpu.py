@@ -53,3 +53,17 @@ def test_cpu_baseline_is_the_oracle(bench, orc):
         assert r["subranges"][k]["T_threads"] > 0 and r["subranges"][k]["1_thread"] > 0
     pv = r["parity_vs_gpu"]
     assert pv["samples"] == 512 and pv["over_tol"] == 0 and pv["max_abs_dh"] < 1e-6
+
+
+def test_line_order_and_summary(bench):
+    """The contract keys lead the JSON line, then the per-config summary."""
+    r = {"value": 147.0, "metric": "m", "unit": "u", "roofline": {"frac": 0.65, "fma_pipe": {"frac": 0.74}},
+         "c3": {"gb_s": 7200.0, "frac_hbm": 1.1, "t_heitz_over_t_cap": 1.0}, "c1": {"cap_us": 1.9},
+         "parity": {"over_tol": 0}, "cpu_baseline": {"value": 0.08}, "extra": 1}
+    o = bench.ordered(r)
+    keys = list(o)
+    assert keys[:4] == ["metric", "value", "unit", "roofline"] and keys[4] == "summary"
+    s = o["summary"]
+    assert s["c4_gsamples_s"] == 147.0 and s["c4_frac_fma_pipe"] == 0.74 and s["c3_gb_s"] == 7200.0
+    assert s["c1_cap_us"] == 1.9 and s["c5_t_heitz_over_t_cap"] is None and s["parity_over_tol"] == 0
+    assert o["extra"] == 1
