@@ -49,5 +49,47 @@ with open(out, "w") as f:
         name = "cap" if "philox_kernel<0" in d["kernel"] else "heitz"
         traffic[f"{name}_philox_c4_warp_inst_per_sample"] = round(ipw, 4)
         traffic[f"{name}_philox_c4_pipes"] = {k: round(float(data[j][hdr.index(v)]) / 100, 4) for k, v in PIPES.items()}
+
+# dynamic opcode counts per sample from the source page -> the FMA-datapath bound
+# (DESIGN.md s.6.5): IMAD.WIDE 4.335 clk, FP32 FMA-pipe instruction 1.03 clk, other
+# IMAD 2 clk per warp-instruction (tools/mix_probe.cu, tools/pipe_probe.cu)
+src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                     capture_output=True).stdout.decode("latin-1")
+rows = list(csv.reader(io.StringIO(src)))
+starts = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"]
+FP32 = ("FFMA", "FMUL", "FADD", "HFMA2", "FMUL.RZ", "FFMA.RZ", "FADD.FTZ", "FMUL.FTZ", "FFMA.FTZ")
+rates = traffic.get("fma_pipe_rates_measured", {"imad_wide_clk": 4.335, "ffma_clk": 1.03, "imad_clk": 2.0})
+with open(out, "a") as f:
+    for k, st in enumerate(starts):
+        end = starts[k + 1] if k + 1 < len(starts) else len(rows)
+        blk = rows[st + 1:end]
+        col = {h: i for i, h in enumerate(blk[0])}
+        ic = [h for h in blk[0] if "Instructions Executed" in h][0]
+        wide = fp = imad = 0.0
+        for r in blk[1:]:
+            if len(r) < len(blk[0]):
+                continue
+            t = r[col["Source"]].split()
+            if not t:
+                continue
+            op = t[1] if t[0].startswith("@") else t[0]
+            try:
+                c = float(r[col[ic]] or 0)
+            except ValueError:
+                continue
+            if op.startswith("IMAD.WIDE"):
+                wide += c
+            elif op.startswith("IMAD"):
+                imad += c
+            elif op in FP32 or op.split(".")[0] in ("FFMA", "FMUL", "FADD", "HFMA2"):
+                fp += c
+        ws = N / 32.0
+        mix = {"IMAD.WIDE.U32": round(wide / ws, 2), "fp32_fma_pipe": round(fp / ws, 2), "IMAD_other": round(imad / ws, 2)}
+        cyc = mix["IMAD.WIDE.U32"] * rates["imad_wide_clk"] + mix["fp32_fma_pipe"] * rates["ffma_clk"] + \
+            mix["IMAD_other"] * rates["imad_clk"]
+        name = "cap" if "(int)0" in rows[st][1] or "philox_kernel<0" in rows[st][1] else "heitz"
+        traffic[f"{name}_philox_c4_fma_mix"] = mix
+        traffic[f"{name}_philox_c4_fma_pipe_cycles_per_warp_sample"] = round(cyc, 1)
+        f.write(f"{name}: per 32 samples {mix} -> FMA datapath {cyc:.1f} clk\n")
 json.dump(traffic, open(tpath, "w"), indent=1)
 print(open(out).read())

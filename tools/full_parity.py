@@ -4,7 +4,7 @@ oracle, in chunks of 2^24 so host memory stays bounded.  The pytest suite
 compares full ranges up to 2^24 and sampled indices beyond; this one-off run
 (a few minutes on the GPU box) closes the gap.
 
-python tools/full_parity.py > profiles/r1/full_parity_r1.txt
+python tools/full_parity.py > profiles/r2/full_parity_r2.txt
 """
 import os
 import sys
@@ -30,14 +30,18 @@ def report(label, n, eh, ep, bad, t0):
           f"over tolerance {bad}  ({time.time() - t0:.0f} s)", flush=True)
 
 
-def streamed(cid, native=False):
+def streamed(cid, native=False, fused_edge=False):
+    """fused_edge: config 5 through vndf_sample_cap_philox_edge (inputs generated
+    in-kernel), checked against the oracle on the recipe's planes."""
     cfg = synth.CONFIGS[cid]
     n = cfg.n if not native else CHUNK  # the native oracle runs binary128, single-threaded: a 2^24 prefix
     t0 = time.time()
     x = synth.fill(cfg.recipe, cfg.seed, n, device=dev)
     out = vndf.empty_outputs(n, dev, pdf=cfg.pdf or native)
     ins = [x[k] for k in synth.PLANES]
-    if native:
+    if fused_edge:
+        vndf.vndf_sample_cap_philox_edge(cfg.seed, 0, n, *out)
+    elif native:
         vndf.vndf_sample_cap_pdf_native(*ins, *out)
     elif cfg.pdf:
         vndf.vndf_sample_cap_pdf(*ins, *out)
@@ -64,7 +68,7 @@ def streamed(cid, native=False):
             ep = max(ep, float(r.max()))
             over |= r > TOL_PDF
         bad += int(over.sum())
-    report(f"config {cid}{' native (2^24 prefix)' if native else ''}", n, eh,
+    report(f"config {cid}{' native (2^24 prefix)' if native else ''}{' fused edge' if fused_edge else ''}", n, eh,
            ep if (cfg.pdf or native) else None, bad, t0)
     del x, out
 
@@ -135,6 +139,7 @@ print(f"# every sample against the float64 oracle; tolerances |dh| <= {TOL_H}, p
 for cid in (1, 2, 3, 5):
     streamed(cid)
 streamed(5, native=True)
+streamed(5, fused_edge=True)
 fused()
 reflect(2)
 reflect(5)
