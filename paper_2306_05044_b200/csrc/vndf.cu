@@ -711,6 +711,18 @@ const void* mapped_pointer(const void* host) {
     if (at.type != cudaMemoryTypeHost || at.devicePointer == nullptr) return nullptr;
     return at.devicePointer;
 }
+
+// Host-path choice (measured on B200, tools/e2e_c4_probe.py): the input+output
+// config-2 path is faster zero-copy (both link directions busy from the SMs,
+// 1.70 vs 1.64 Gsamples/s), the output-only config-4 path through DMA staging
+// (3.35 vs 3.16).  Measurement hook: VNDF_HOST_ZERO_COPY=0 / =1 forces the
+// staged / zero-copy path for mapped page-locked buffers in both.
+bool zero_copy_allowed(bool dflt) {
+    const char* v = getenv("VNDF_HOST_ZERO_COPY");
+    if (v && v[0] == '0') return false;
+    if (v && v[0] == '1') return true;
+    return dflt;
+}
 }  // namespace
 
 extern "C" {
@@ -731,7 +743,7 @@ vndf_status vndf_sample_cap_pdf_host(const float* wi_x, const float* wi_y, const
     {
         const void* hp[11] = {wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, h_x, h_y, h_z, pdf};
         const void* dp[11];
-        bool mapped = true;
+        bool mapped = zero_copy_allowed(true);
         for (int k = 0; k < 11 && mapped; ++k) mapped = (dp[k] = mapped_pointer(hp[k])) != nullptr;
         if (mapped) {
             const StreamArgs da = make_args((const float*)dp[0], (const float*)dp[1], (const float*)dp[2],
@@ -791,11 +803,11 @@ vndf_status vndf_sample_cap_philox_host(uint64_t seed, uint64_t first_index, int
     cudaStream_t user = (cudaStream_t)stream;
     float* hout[4] = {h_x, h_y, h_z, pdf};
     const int nout = pdf ? 4 : 3;
-    // Zero-copy: mapped page-locked outputs are written by the kernel across
-    // the host link in place (16 B per sample device -> host, nothing in).
+    // Zero-copy (only when forced: the DMA staging below is faster for this
+    // output-only path): mapped page-locked outputs written by the kernel.
     {
         void* dp[4] = {nullptr, nullptr, nullptr, nullptr};
-        bool mapped = true;
+        bool mapped = zero_copy_allowed(false);
         for (int k = 0; k < nout && mapped; ++k) mapped = (dp[k] = (void*)mapped_pointer(hout[k])) != nullptr;
         if (mapped) {
             st = launch_philox<kCap>(seed, first_index, n, (float*)dp[0], (float*)dp[1], (float*)dp[2],
@@ -805,10 +817,10 @@ vndf_status vndf_sample_cap_philox_host(uint64_t seed, uint64_t first_index, int
             return es == cudaSuccess ? VNDF_OK : cuda_fail(es);
         }
     }
-    // Otherwise: chunks through device staging, kernel then device -> host
-    // copies, round-robin over the staging streams.  With pageable outputs
-    // each copy completes before the next call returns, so chunks do not
-    // overlap their copies (pin the outputs for the zero-copy path above).
+    // Chunks through device staging, kernel then device -> host copies,
+    // round-robin over the staging streams: with page-locked outputs the DMA of
+    // one chunk overlaps the kernels of the next; pageable copies complete
+    // before the call returns, so those chunks do not overlap.
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e);

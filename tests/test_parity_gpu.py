@@ -323,8 +323,9 @@ def test_host_entry_point_matches_device(env):
 
 def test_philox_host_entry_point_matches_device(env):
     """vndf_sample_cap_philox_host (config-4 end to end, host outputs) is bit
-    identical to vndf_sample_cap_philox: pinned (zero-copy), pageable (staged
-    chunks, ragged), and without pdf."""
+    identical to vndf_sample_cap_philox: pinned and pageable outputs (staged
+    chunks, ragged), and without pdf (the forced zero-copy path:
+    test_host_paths_gpu.py)."""
     oracle, vndf, synth, dev = env
     n = (1 << 22) + 2 ** 21 + 13     # three staging chunks, ragged
     first = 2**32 - 1000             # the 32-bit counter carry inside the call
