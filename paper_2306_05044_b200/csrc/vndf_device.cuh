@@ -222,7 +222,8 @@ __device__ __forceinline__ bool cap_reflect_fp32(float wx, float wy, float wz, f
 
 // ---------------------------------------------------------------------------
 // Float64 recomputation of one cap sample (the fix-up).  Same algebra as
-// cap_fp32, in double throughout (sincospi, sqrt, rsqrt, division).
+// cap_fp32 in double (sincospi, sqrt, rsqrt) up to m and hs; the final
+// normalisation and the pdf in fp32 (see below).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ float4 cap_fp64_d(double wx, double wy, double wz, double ax, double ay,
                                              double u1, double u2, bool flip = true) {
@@ -247,11 +248,24 @@ __device__ __forceinline__ float4 cap_fp64_d(double wx, double wy, double wz, do
     const double hx = fma(st, cp, wsx), hy = fma(st, sp, wsy);
     const double mx = ax * hx, my = ay * hy;
     const double m2 = mx * mx + my * my + hz * hz;
-    const double iN = rsqrt(m2);
     const double hs2 = hx * hx + hy * hy + hz * hz;
-    const double pdf = m2 * m2 * iN / (kPiD * ax * ay * a * hs2);
-    const double t = s * iN;
-    return make_float4((float)(mx * t), (float)(my * t), (float)(hz * t), (float)pdf);
+    // The cancellation is behind us: m and hs carry float64 accuracy, and the
+    // normalisation and the pdf are products and quotients of them -- well
+    // conditioned -- so they run in fp32 (MUFU rsqrt / rcp, relative error
+    // ~1e-7, far inside 2e-5 / 1e-4) instead of a dependent float64 rsqrt and
+    // division (~230 of the recomputation's 575 clocks, tools/fix_latency.cu).
+    // An exact power-of-two scale 2^-k brings |hs|^2 into [1, 4) (and |m|^2,
+    // <= max(1, a)^2 |hs|^2, with it), so nothing under- or overflows fp32;
+    // pdf = |m|^3 / (pi ax ay a |hs|^2) then carries the factor 2^k.
+    const int k = (((__double2hiint(hs2) >> 20) & 0x7ff) - 1023) >> 1;  // floor(floor(log2 |hs|^2) / 2)
+    const double sc = __hiloint2double((1023 - k) << 20, 0);           // 2^-k
+    const float mxs = (float)(mx * sc), mys = (float)(my * sc), hzs = (float)(hz * sc);
+    const float m2s = (float)(m2 * sc * sc), hs2s = (float)(hs2 * sc * sc);
+    const float iN = rsqrt_approx(m2s);
+    const float t = (float)s * iN;
+    const float den = (kPiF * (float)ax * (float)ay) * (float)a * hs2s;
+    const float pdf = m2s * (m2s * iN) * rcp_approx(den) * __int_as_float((127 + k) << 23);
+    return make_float4(mxs * t, mys * t, hzs * t, pdf);
 }
 
 // Float64 reflection sample (fix-up of cap_reflect_fp32), same formulas.
