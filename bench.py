@@ -497,12 +497,43 @@ def run_ours(args):
         cb = cpu_baseline(check=(check_i, check_h, check_p), c1_planes=c1p, c3_planes=c3p)
         result["parity"] = cb.pop("parity_vs_gpu")
         result["cpu_baseline"] = cb
+        result["chi2"] = chi2_pvalues(torch, vndf, synth, dev)
     elif rank == 0:
         result["cpu_baseline"] = None
     if rank == 0:
         print(json.dumps(ordered(result), separators=(",", ":")), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+CHI2_PAIRS = [(0, 0, 1, 1), (0, 0, .5, .5), (45, 0, .2, .2), (80, 30, .5, .5),
+              (70, 20, .05, .3), (85, 60, .3, .05), (45, 0, .01, .01), (60, 135, 1, .1)]
+
+
+def chi2_pvalues(torch, vndf, synth, dev, n: int = 1 << 21, seed: int = 1000):
+    """BJ config 2's distribution check in the bench run: 64 x 64 (theta, phi)
+    histograms of h from the cap and Heitz kernels, 2^21 samples for each of the
+    eight fixed (wi, alpha) pairs, Pearson chi-square against the oracle's Eq. 1
+    quadrature masses (reading R14; tests/test_distribution_gpu.py
+    holds the 3-seed gate)."""
+    import numpy as np
+    from oracle import stats
+    out = {"n_per_pair": n, "seed": seed, "pairs_theta_phi_ax_ay": CHI2_PAIRS, "cap_p": [], "heitz_p": []}
+    for t, p, ax, ay in CHI2_PAIRS:
+        tr, pr = np.radians(t), np.radians(p)
+        wi = np.array([np.sin(tr) * np.cos(pr), np.sin(tr) * np.sin(pr), np.cos(tr)], dtype=np.float32)
+        masses = stats.bin_masses(wi.astype(np.float64), ax, ay)
+        x = synth.fill(0, seed, n, device=dev, fixed=[wi[0], wi[1], wi[2], ax, ay])
+        ins = [x[k] for k in synth.PLANES]
+        o = vndf.empty_outputs(n, dev)
+        for name, fn in (("cap_p", vndf.vndf_sample_cap_pdf), ("heitz_p", vndf.vndf_sample_heitz2018)):
+            fn(*ins, *o)
+            torch.cuda.synchronize()
+            h = np.stack([q.cpu().numpy() for q in o[:3]]).astype(np.float64)
+            _, _, pv = stats.pearson(stats.histogram(h), masses)
+            out[name].append(float(f"{pv:.3g}"))
+    out["cap_min_p"], out["heitz_min_p"] = min(out["cap_p"]), min(out["heitz_p"])
+    return out
 
 
 CONTRACT_KEYS = ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
@@ -527,7 +558,8 @@ def summary(r):
             "c1_cap_us": g("c1", "cap_us"), "c1_t_heitz_over_t_cap": g("c1", "t_heitz_over_t_cap"),
             "c2_frac_hbm": g("c2", "frac_hbm"),
             "sampler_only_t_heitz_over_t_cap": g("next", "microbench_t_heitz_over_t_cap"),
-            "parity_over_tol": g("parity", "over_tol"), "cpu_oracle_gsamples_s": g("cpu_baseline", "value")}
+            "parity_over_tol": g("parity", "over_tol"), "chi2_cap_min_p": g("chi2", "cap_min_p"),
+            "cpu_oracle_gsamples_s": g("cpu_baseline", "value")}
 
 
 def ordered(r):
