@@ -257,13 +257,14 @@ def issue_roofline(gsamples_s: float, key: str, n_per_launch: int = None, launch
            "model": "592 SMSPs x 1 warp-inst/clk x 1965 MHz; ncu warp-inst/sample (DESIGN.md s.6.4)"}
     # the FMA datapath: IMAD.WIDE.U32 (Philox) holds it ~4.3 clk per warp-instruction
     # and does not overlap with FP32 FFMA/FMUL on B200 (tools/mix_probe.cu), so the
-    # sum of the measured per-instruction costs bounds the kernel (DESIGN.md s.6.4)
+    # sum of the measured per-instruction costs bounds the kernel (DESIGN.md s.6.5)
     cyc = _profiled(key.replace("warp_inst_per_sample", "fma_pipe_cycles_per_warp_sample"))
     if cyc:
         bound = SMS * SMSPS_PER_SM * f * 32 / cyc / 1e9
         out["fma_pipe"] = {"cycles_per_warp_sample": cyc, "gsamples_s_bound": round(bound, 2),
                            "frac": round(gsamples_s / bound, 4),
-                           "model": "measured clk per IMAD.WIDE / FP32 / IMAD x ncu counts (DESIGN.md s.6.4)"}
+                           "model": "measured clk per IMAD.WIDE / FFMA 3-reg / other FP32 / IMAD x ncu counts "
+                                    "(DESIGN.md s.6.5)"}
     return out
 
 

@@ -58,14 +58,30 @@ src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-so
 rows = list(csv.reader(io.StringIO(src)))
 starts = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"]
 FP32 = ("FFMA", "FMUL", "FADD", "HFMA2", "FMUL.RZ", "FFMA.RZ", "FADD.FTZ", "FMUL.FTZ", "FFMA.FTZ")
-rates = traffic.get("fma_pipe_rates_measured", {"imad_wide_clk": 4.335, "ffma_clk": 1.03, "imad_clk": 2.0})
+rates = traffic.get("fma_pipe_rates_measured", {})
+rates.setdefault("imad_wide_clk", 4.335)
+rates.setdefault("ffma_clk", 1.03)          # FMUL, FADD, FFMA with an immediate or constant operand
+rates.setdefault("ffma_3reg_clk", 1.52)     # FFMA with three register sources (tools/pipe_probe.cu: 0.656/clk)
+rates.setdefault("imad_clk", 2.0)
+traffic["fma_pipe_rates_measured"] = rates
+
+
+def _three_regs(src: str) -> bool:
+    """FFMA Rd, Ra, Rb, Rc (no immediate, constant-bank or RZ source)."""
+    ops = src.split(None, 1)[1] if " " in src else ""
+    args = [a.strip().lstrip("-|").rstrip("|") for a in ops.rstrip(";").split(",")]
+    return len(args) == 4 and all(a.startswith("R") and a != "RZ" for a in args[1:])
+done = set()
 with open(out, "a") as f:
     for k, st in enumerate(starts):
+        if rows[st][1] in done:     # the source page may list a kernel more than once
+            continue
+        done.add(rows[st][1])
         end = starts[k + 1] if k + 1 < len(starts) else len(rows)
         blk = rows[st + 1:end]
         col = {h: i for i, h in enumerate(blk[0])}
         ic = [h for h in blk[0] if "Instructions Executed" in h][0]
-        wide = fp = imad = 0.0
+        wide = fp = fp3 = imad = 0.0
         for r in blk[1:]:
             if len(r) < len(blk[0]):
                 continue
@@ -81,12 +97,15 @@ with open(out, "a") as f:
                 wide += c
             elif op.startswith("IMAD"):
                 imad += c
+            elif op.split(".")[0] == "FFMA" and _three_regs(" ".join(t[1:] if t[0].startswith("@") else t)):
+                fp3 += c
             elif op in FP32 or op.split(".")[0] in ("FFMA", "FMUL", "FADD", "HFMA2"):
                 fp += c
         ws = N / 32.0
-        mix = {"IMAD.WIDE.U32": round(wide / ws, 2), "fp32_fma_pipe": round(fp / ws, 2), "IMAD_other": round(imad / ws, 2)}
+        mix = {"IMAD.WIDE.U32": round(wide / ws, 2), "fp32_fma_pipe": round(fp / ws, 2),
+               "ffma_3reg": round(fp3 / ws, 2), "IMAD_other": round(imad / ws, 2)}
         cyc = mix["IMAD.WIDE.U32"] * rates["imad_wide_clk"] + mix["fp32_fma_pipe"] * rates["ffma_clk"] + \
-            mix["IMAD_other"] * rates["imad_clk"]
+            mix["ffma_3reg"] * rates["ffma_3reg_clk"] + mix["IMAD_other"] * rates["imad_clk"]
         name = "cap" if "(int)0" in rows[st][1] or "philox_kernel<0" in rows[st][1] else "heitz"
         traffic[f"{name}_philox_c4_fma_mix"] = mix
         traffic[f"{name}_philox_c4_fma_pipe_cycles_per_warp_sample"] = round(cyc, 1)
