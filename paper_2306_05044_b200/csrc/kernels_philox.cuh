@@ -127,24 +127,32 @@ __device__ __forceinline__ void block_queue_flush(const FixQueue& fq, BlockQueue
 
 // ctr = first + k, the Philox counter of local sample k; returns the
 // conditioning flag (always false for Heitz)
-template <int METHOD, bool PDF, int RECIPE = kRecipeC4>
-__device__ __forceinline__ bool philox_one(const PhiloxKeys& ks, uint64_t ctr, Sample& o) {
+// One sample from its two blocks of Philox words; returns the conditioning
+// flag (always false for Heitz).
+template <int METHOD, bool PDF, int RECIPE>
+__device__ __forceinline__ bool sample_words(uint4 X, uint4 Y, Sample& o) {
     if (RECIPE == kRecipeC5) {
         // edge mix: back-side incidence is flipped (reading R4), as in the streamed kernels
-        uint4 X, Y;
-        philox_pair_ks(ks, ctr, X, Y);
         const Inputs in = c5_inputs_fp32(X, Y);
         if (METHOD == kCap) return cap_fp32<PDF>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o);
         heitz_fp32<PDF>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, o);
         return false;
     }
-    const Inputs in = c4_inputs_ks<VNDF_CAP_FW_HI && METHOD == kCap>(ks, ctr);
+    const Inputs in = c4_inputs_fp32<VNDF_CAP_FW_HI && METHOD == kCap>(X, Y);
     if (METHOD == kCap) {
         // config-4 inputs are on the upper hemisphere (wi.z = 1 - u > 0): no flip
         return cap_fp32<PDF, kFrameUpper>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o);
     }
     heitz_fp32<PDF, false>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, o);
     return false;
+}
+
+// ctr = first + k, the Philox counter of local sample k
+template <int METHOD, bool PDF, int RECIPE = kRecipeC4>
+__device__ __forceinline__ bool philox_one(const PhiloxKeys& ks, uint64_t ctr, Sample& o) {
+    uint4 X, Y;
+    philox_pair_ks(ks, ctr, X, Y);
+    return sample_words<METHOD, PDF, RECIPE>(X, Y, o);
 }
 
 template <int RECIPE>
@@ -219,13 +227,21 @@ __global__ void __launch_bounds__(PhiloxLaunch<METHOD>::kBlock, PhiloxLaunch<MET
     for (int64_t c = tid; c < nchunks; c += stride) {
         const int64_t i = c * V;
         const uint64_t base = first + (uint64_t)i;
+        // aligned chunks: round 0's product M0 i_lo once per chunk (philox_pair_r0)
+        const uint64_t p0 = (uint64_t)0xD2511F53u * (uint32_t)base;
         Vec<V> hx, hy, hz, pd;
         unsigned flags = 0;
 #pragma unroll
         for (int j = 0; j < V; ++j) {
-            const uint64_t ctr = ALIGNED ? (base | (uint64_t)j) : base + (uint64_t)j;
             Sample o;
-            flags |= (unsigned)philox_one<METHOD, PDF, RECIPE>(ks, ctr, o) << j;
+            if (ALIGNED && V <= 8) {
+                uint4 X, Y;
+                philox_pair_r0(ks, p0 + (uint64_t)0xD2511F53u * (uint32_t)j, (uint32_t)(base >> 32), X, Y);
+                flags |= (unsigned)sample_words<METHOD, PDF, RECIPE>(X, Y, o) << j;
+            } else {
+                const uint64_t ctr = ALIGNED ? (base | (uint64_t)j) : base + (uint64_t)j;
+                flags |= (unsigned)philox_one<METHOD, PDF, RECIPE>(ks, ctr, o) << j;
+            }
             hx.v[j] = o.x;
             hy.v[j] = o.y;
             hz.v[j] = o.z;

@@ -558,6 +558,26 @@ __device__ __forceinline__ void philox_pair_ks(const PhiloxKeys& ks, uint64_t i,
     Y = y;
 }
 
+// The same two blocks from round 0's shared product p0 = M0 i_lo (64-bit) and
+// i_hi.  Round 0 of counter (i_lo, i_hi, b, 0) leaves x = (i_hi ^ k0, lo(M1 b),
+// hi(p0) ^ k1, lo(p0)) with M1 b = 0 (b = 0) or M1 (b = 1), so after it the
+// blocks differ in one word; rounds 1-9 as in philox_pair_ks.  For the counters
+// base + j of a chunk with base = 0 mod 8 and j < 8 (no carry into i_hi),
+// M0 (base_lo + j) = M0 base_lo + M0 j exactly: one IMAD.WIDE per chunk and a
+// 64-bit add per sample replace a multiply per sample on the FMA datapath.
+__device__ __forceinline__ void philox_pair_r0(const PhiloxKeys& ks, uint64_t p0, uint32_t i_hi, uint4& X,
+                                               uint4& Y) {
+    uint4 x = make_uint4(i_hi ^ ks.k0[0], 0u, (uint32_t)(p0 >> 32) ^ ks.k1[0], (uint32_t)p0);
+    uint4 y = make_uint4(i_hi ^ ks.k0[0], 0xCD9E8D57u, (uint32_t)(p0 >> 32) ^ ks.k1[0], (uint32_t)p0);
+#pragma unroll
+    for (int r = 1; r < 10; ++r) {
+        x = philox_round(x, ks.k0[r], ks.k1[r]);
+        y = philox_round(y, ks.k0[r], ks.k1[r]);
+    }
+    X = x;
+    Y = y;
+}
+
 __device__ __forceinline__ uint4 philox_block(uint64_t seed, uint64_t i, uint32_t block) {
     return philox4x32_10(make_uint4((uint32_t)i, (uint32_t)(i >> 32), block, 0u),
                          make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
