@@ -40,7 +40,7 @@ constexpr double kPiD = 3.14159265358979323846;
 // The fused kernel (kFrameUpper, config 4) keeps the earlier scale-free test
 // (A = max(a)/|m| <= 30, B = 1/|hs| <= 40; calibrated with tools/calibrate_flags.py):
 // its inputs never reach the small-S regime and it saves two instructions.
-constexpr float kFlagM = 1.0f / 900.0f;    // scale-free A <= 30 (kFrameUpper)
+constexpr float kFlagA = 30.0f;            // scale-free A <= 30 (kFrameUpper)
 constexpr float kFlagHs = 1.0f / 1600.0f;  // scale-free B <= 40 (kFrameUpper)
 constexpr float kFlagMS = 2.0f / 1600.0f;  // scaled: m2 < max(a)^2 * 2 (sin2 + rs2) / 40^2
 constexpr float kFlagHsS = 2.0f / 3600.0f; // scaled: hs2 < 2 (sin2 + rs2) / 60^2
@@ -162,7 +162,9 @@ __device__ __forceinline__ bool cap_flag(const CapCore& k, float ax, float ay) {
     return false;
 #else
     const float amax = fmaxf(ax, ay);
-    if (FRAME == kFrameUpper) return (k.m2 < kFlagM * (amax * amax)) | (k.hs2 < kFlagHs);
+    // A = max(a)/|m| > 30 from the 1/|m| the normalisation already has: one
+    // multiply fewer on the fused kernel's FMA datapath than m2 < max(a)^2/900
+    if (FRAME == kFrameUpper) return (amax * k.invN > kFlagA) | (k.hs2 < kFlagHs);
     return (k.m2 < kFlagMS * (amax * amax) * k.s2) | (k.hs2 < kFlagHsS * k.s2);
 #endif
 }
