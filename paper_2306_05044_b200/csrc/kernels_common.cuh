@@ -128,9 +128,12 @@ __device__ __forceinline__ bool sample_one(float wx, float wy, float wz, float a
 
 // Float64 recomputation of a flagged sample from its fp32 inputs (flip: the
 // flip frame of reading R4, else the native frame).
+// INLINE: the float64 arithmetic inlined (cap_fp64_d) rather than called
+// out of line (cap_fp64).
+template <bool INLINE>
 __device__ __forceinline__ Sample fix_regs(float wx, float wy, float wz, float ax, float ay, float u1, float u2,
                                            bool flip) {
-    const float4 f = cap_fp64(wx, wy, wz, ax, ay, u1, u2, flip);
+    const float4 f = INLINE ? cap_fp64_d(wx, wy, wz, ax, ay, u1, u2, flip) : cap_fp64(wx, wy, wz, ax, ay, u1, u2, flip);
     Sample o;
     o.x = f.x;
     o.y = f.y;

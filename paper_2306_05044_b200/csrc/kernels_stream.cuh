@@ -9,8 +9,11 @@
 // path (one chunk per thread by default, grid-stride if the grid is capped);
 // the n mod V tail is done by the first threads of the grid with scalar
 // accesses.  A flagged sample is recomputed in float64 at once, in the thread
-// that found it, from the inputs it holds in registers (cap_fp64, an
-// out-of-line call, so the vector loop keeps its registers).  Round 1 pushed
+// that found it, from the inputs it holds in registers: inlined in the 4-sample
+// loop of small, latency-bound calls (config 1: 1.89 -> 1.72 us per launch, the
+// call's ~80 clocks and the scheduling barrier it puts in the loop gone), an
+// out-of-line call (cap_fp64) in the 8-sample loop (inlined there it measured
+// 3% slower at 2^20 samples).  Round 1 pushed
 // flagged samples to a shared-memory queue, recomputed after a block barrier
 // from a reload of their inputs; inline is faster wherever it was measured
 // (config 5: 7.12 vs 6.86 TB/s; config 1: 2.54 vs 2.81 us per launch -- the
@@ -44,7 +47,7 @@ __global__ void __launch_bounds__(VNDF_STREAM_BOUND, VNDF_STREAM_MINB) stream_ke
         for (int j = 0; j < V; ++j) {
             Sample o;
             if (sample_one<METHOD, PDF>(wx.v[j], wy.v[j], wz.v[j], ax.v[j], ay.v[j], u1.v[j], u2.v[j], o))
-                o = fix_regs(wx.v[j], wy.v[j], wz.v[j], ax.v[j], ay.v[j], u1.v[j], u2.v[j], METHOD == kCap);
+                o = fix_regs<(V <= 4)>(wx.v[j], wy.v[j], wz.v[j], ax.v[j], ay.v[j], u1.v[j], u2.v[j], METHOD == kCap);
             hx.v[j] = o.x;
             hy.v[j] = o.y;
             hz.v[j] = o.z;
@@ -62,7 +65,7 @@ __global__ void __launch_bounds__(VNDF_STREAM_BOUND, VNDF_STREAM_MINB) stream_ke
                         u2 = a.u2[i];
             Sample o;
             if (sample_one<METHOD, PDF>(wx, wy, wz, ax, ay, u1, u2, o))
-                o = fix_regs(wx, wy, wz, ax, ay, u1, u2, METHOD == kCap);
+                o = fix_regs<false>(wx, wy, wz, ax, ay, u1, u2, METHOD == kCap);
             a.hx[i] = o.x;
             a.hy[i] = o.y;
             a.hz[i] = o.z;
