@@ -1,6 +1,6 @@
 """Small driver for ncu captures: a few launches of each hot kernel.
 
-python tools/prof_kernels.py [which]   which in {all, c2, c3, c4, c5, c5fused, reflect_philox, next}
+python tools/prof_kernels.py [which]   which in {all, c2, c3, c4, c4full, c5, c5fused, reflect_philox, next}
 """
 import os
 import sys
@@ -37,6 +37,12 @@ if which in ("all", "c4"):
     for _ in range(2):
         vndf.vndf_sample_cap_philox(3, 0, n, *o)
         vndf.vndf_sample_heitz2018_philox(3, 0, n, *o)
+    torch.cuda.synchronize()
+if which == "c4full":  # the bench step's launch shape: 2^30 samples, one call each
+    n = 1 << 30
+    o = vndf.empty_outputs(n, dev)
+    vndf.vndf_sample_cap_philox(3, 0, n, *o)
+    vndf.vndf_sample_heitz2018_philox(3, 0, n, *o)
     torch.cuda.synchronize()
 if which in ("all", "c5fused"):
     n = 1 << 26
