@@ -619,7 +619,19 @@ def side_runs(torch, vndf, synth, dev, stream, c4_value):
     res["c3"] = {"gsamples_s": gs(c3.n, t_cap3), "ms": round(t_cap3, 4), "gb_s": rl3["achieved"],
                  "frac_hbm": rl3["frac"], "t_heitz_over_t_cap": round(t_hz3 / t_cap3, 4), "roofline": rl3,
                  "inputs_sha256_first_2e20": _sha256(ins3, 1 << 20)[:16]}
+    # config 3 end to end: pinned host planes in (28 B) and out (12 B), zero-copy
+    hin3 = [t.cpu().pin_memory() for t in ins3]
     del x3, o3, ins3
+    torch.cuda.empty_cache()
+    hout3 = [torch.empty(c3.n, dtype=torch.float32, pin_memory=True) for _ in range(3)]
+    vndf.vndf_sample_cap_pdf_host(*hin3, *hout3, None)
+    t0 = time.perf_counter()
+    for _ in range(3):
+        vndf.vndf_sample_cap_pdf_host(*hin3, *hout3, None)
+    e3 = (time.perf_counter() - t0) / 3
+    res["c3"]["e2e"] = {"gsamples_s": round(c3.n / e3 / 1e9, 4), "link_gb_s": round(40 * c3.n / e3 / 1e9, 2),
+                        "api": "vndf_sample_cap_pdf_host (pdf NULL, zero-copy)"}
+    del hin3, hout3
     torch.cuda.empty_cache()
 
     # config 5: 2^26 edge mix, h + pdf (flip frame and the native frame)

@@ -167,7 +167,8 @@ vndf_status vndf_sample_heitz2018_philox_edge(uint64_t seed, uint64_t first_inde
 vndf_status vndf_philox4x32_10(uint64_t seed, uint64_t first_index, int64_t n,
                                uint32_t block, uint32_t *words, vndf_stream_t stream);
 
-/* End-to-end form of vndf_sample_cap_pdf on HOST buffers.
+/* End-to-end form of vndf_sample_cap_pdf on HOST buffers; pdf may be NULL
+ * (h only: the end-to-end form of vndf_sample_cap, BASELINE config 3).
  * - If all eleven buffers are page-locked and mapped into the device's address
  *   space (cudaHostAlloc / cudaMallocHost / torch pin_memory(); mapped by
  *   default under unified addressing), the kernel reads the inputs and writes

@@ -270,10 +270,11 @@ def vndf_count_fixups_philox(seed, first_index, n, count, stream=None):
            lib().vndf_count_fixups_philox(int(seed), int(first_index), int(n), c, _stream(stream, dev)))
 
 
-def vndf_sample_cap_pdf_host(wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, h_x, h_y, h_z, pdf,
+def vndf_sample_cap_pdf_host(wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, h_x, h_y, h_z, pdf=None,
                              n=None, stream=None):
     """End-to-end call on HOST buffers (CPU torch tensors, ideally pinned, or
-    numpy arrays); blocking.  Copies and kernel overlap inside libvndf."""
+    numpy arrays); blocking.  Copies and kernel overlap inside libvndf.
+    pdf=None: h only (config 3's end-to-end form)."""
     import numpy as np
     import torch
     arrs = (wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, h_x, h_y, h_z, pdf)
@@ -281,7 +282,9 @@ def vndf_sample_cap_pdf_host(wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, h_x, h_
     n = int(len(wi_x)) if n is None else int(n)
     ptrs = []
     for a, nm in zip(arrs, names):
-        if isinstance(a, torch.Tensor):
+        if a is None and nm == "pdf":
+            ptrs.append(ctypes.c_void_p(0))
+        elif isinstance(a, torch.Tensor):
             if a.is_cuda or a.dtype != torch.float32 or not a.is_contiguous() or a.numel() < n:
                 raise ValueError(f"{nm}: expected a contiguous float32 CPU tensor of >= {n} elements")
             ptrs.append(ctypes.c_void_p(a.data_ptr()))

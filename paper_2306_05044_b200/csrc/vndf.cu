@@ -733,24 +733,25 @@ vndf_status vndf_sample_cap_pdf_host(const float* wi_x, const float* wi_y, const
                                      int64_t n, vndf_stream_t stream) {
     DeviceGuard device_guard((cudaStream_t)stream);
     const StreamArgs host = make_args(wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, h_x, h_y, h_z, pdf);
-    vndf_status st = validate_stream(host, true, n);
+    vndf_status st = validate_stream(host, false, n);
     if (st != VNDF_OK || n == 0) return st;
     cudaStream_t user = (cudaStream_t)stream;
+    const int nbuf = pdf ? 11 : 10;  // pdf NULL: h only (BASELINE config 3's 28 B in, 12 B out)
     // Zero-copy: when all eleven buffers are mapped page-locked memory, the
     // kernel reads its inputs and writes its outputs across the host link in
     // place -- no copies, no staging; reads and writes overlap in both link
     // directions (1.72 vs 1.65 Gsamples/s staged, tools/e2e_probe.py).
     {
         const void* hp[11] = {wi_x, wi_y, wi_z, alpha_x, alpha_y, u1, u2, h_x, h_y, h_z, pdf};
-        const void* dp[11];
+        const void* dp[11] = {};
         bool mapped = zero_copy_allowed(true);
-        for (int k = 0; k < 11 && mapped; ++k) mapped = (dp[k] = mapped_pointer(hp[k])) != nullptr;
+        for (int k = 0; k < nbuf && mapped; ++k) mapped = (dp[k] = mapped_pointer(hp[k])) != nullptr;
         if (mapped) {
             const StreamArgs da = make_args((const float*)dp[0], (const float*)dp[1], (const float*)dp[2],
                                             (const float*)dp[3], (const float*)dp[4], (const float*)dp[5],
                                             (const float*)dp[6], (float*)dp[7], (float*)dp[8], (float*)dp[9],
                                             (float*)dp[10]);
-            st = launch_stream<kCap, true>(da, n, user);
+            st = pdf ? launch_stream<kCap, true>(da, n, user) : launch_stream<kCap, false>(da, n, user);
             if (st != VNDF_OK) return st;
             const cudaError_t es = cudaStreamSynchronize(user);
             return es == cudaSuccess ? VNDF_OK : cuda_fail(es);
@@ -778,9 +779,10 @@ vndf_status vndf_sample_cap_pdf_host(const float* wi_x, const float* wi_y, const
         for (int k = 0; k < 7 && e == cudaSuccess; ++k)
             e = cudaMemcpyAsync(d[k], hin[k] + off, bytes, cudaMemcpyHostToDevice, s);
         if (e != cudaSuccess) break;
-        const StreamArgs da = make_args(d[0], d[1], d[2], d[3], d[4], d[5], d[6], d[7], d[8], d[9], d[10]);
-        result = launch_stream<kCap, true>(da, m, s);
-        for (int k = 0; k < 4 && e == cudaSuccess && result == VNDF_OK; ++k)
+        const StreamArgs da = make_args(d[0], d[1], d[2], d[3], d[4], d[5], d[6], d[7], d[8], d[9],
+                                        pdf ? d[10] : nullptr);
+        result = pdf ? launch_stream<kCap, true>(da, m, s) : launch_stream<kCap, false>(da, m, s);
+        for (int k = 0; k < nbuf - 7 && e == cudaSuccess && result == VNDF_OK; ++k)
             e = cudaMemcpyAsync(hout[k] + off, d[7 + k], bytes, cudaMemcpyDeviceToHost, s);
     }
     // join both pipeline streams back into the caller's stream, then block

@@ -319,6 +319,14 @@ def test_host_entry_point_matches_device(env):
     vndf.vndf_sample_cap_pdf_host(*hin, *mout)
     for a, b in zip(d, mout):
         np.testing.assert_array_equal(a.cpu().numpy(), b)
+    # h only (pdf = NULL: config 3's end-to-end form), zero-copy and staged
+    h3 = [torch.empty(n, dtype=torch.float32).pin_memory() for _ in range(3)]
+    vndf.vndf_sample_cap_pdf_host(*hin, *h3, None)
+    n3 = [np.empty(n, dtype=np.float32) for _ in range(3)]
+    vndf.vndf_sample_cap_pdf_host(*nin, *n3, None)
+    for a, b, c in zip(d[:3], h3, n3):
+        assert torch.equal(a.cpu(), b)
+        np.testing.assert_array_equal(a.cpu().numpy(), c)
 
 
 def test_philox_host_entry_point_matches_device(env):
