@@ -188,10 +188,10 @@ __global__ void __launch_bounds__(128) philox_fixup_kernel(uint64_t seed, uint64
 // store per output plane).  Block sizes / resident blocks per SM are build
 // knobs swept on B200 (tools/build_variant.py + tools/variants.py).
 #ifndef VNDF_PHILOX_BLOCK_CAP
-#define VNDF_PHILOX_BLOCK_CAP 256
+#define VNDF_PHILOX_BLOCK_CAP 512
 #endif
 #ifndef VNDF_PHILOX_BLOCK_HEITZ
-#define VNDF_PHILOX_BLOCK_HEITZ 256
+#define VNDF_PHILOX_BLOCK_HEITZ 512
 #endif
 #ifndef VNDF_PHILOX_MINB_CAP
 #define VNDF_PHILOX_MINB_CAP 1
