@@ -6,9 +6,8 @@
 #pragma once
 
 // Uniform conversion of the cap kernel: 0 = SHF (ALU pipe), 1 = IMAD.HI shifts
-// (fw_hi, FMA-heavy pipe).  1 won with three 256-thread blocks per SM (ALU
-// pipe busier); with one 768-thread block per SM the FMA-heavy pipe is the
-// busier one and 0 is 2.5% faster (tools/variants.py).
+// (fw_hi, FMA pipe).  The FMA datapath is the fused kernel's bound (DESIGN.md
+// s.6.5), so 0: 145.7 vs 141.8 Gsamples/s with 1 (tools/variants.py).
 #ifndef VNDF_CAP_FW_HI
 #define VNDF_CAP_FW_HI 0
 #endif
@@ -185,8 +184,10 @@ __global__ void __launch_bounds__(128) philox_fixup_kernel(uint64_t seed, uint64
 }
 
 // Persistent grid (SMs x resident blocks); 8 samples per thread (one 256-bit
-// store per output plane).  Block sizes / resident blocks per SM are build
-// knobs swept on B200 (tools/build_variant.py + tools/variants.py).
+// store per output plane); 512-thread blocks, one per SM at ~123 registers
+// (1.4% faster than two 256-thread blocks with the same 16 warps per SM).
+// Block sizes / resident blocks per SM are build knobs swept on B200
+// (tools/build_variant.py + tools/variants.py, profiles/r2/fused_variants_r2.txt).
 #ifndef VNDF_PHILOX_BLOCK_CAP
 #define VNDF_PHILOX_BLOCK_CAP 512
 #endif
