@@ -142,6 +142,12 @@ def test_config4_philox_sampled(env):
     eh, ep = _errors(hg, out[3][ti].cpu().numpy(), h_ref, p_ref)
     assert eh.max() <= TOL_H and ep.max() <= TOL_PDF, (float(eh.max()), float(ep.max()))
     assert bool(torch.isfinite(out[3]).all()) and float(out[3].min()) > 0
+    # properties at any size, on EVERY sample: unit h on the upper hemisphere
+    # (config-4 incidence is upper-hemisphere, so h.z >= 0 without a flip)
+    nrm = out[0].double().square_() + out[1].double().square_() + out[2].double().square_()
+    assert float((nrm - 1.0).abs().max()) < 1e-6
+    del nrm
+    assert float(out[2].min()) >= 0.0
     del out
     torch.cuda.empty_cache()
 
