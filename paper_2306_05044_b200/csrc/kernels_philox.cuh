@@ -57,8 +57,9 @@ __device__ __forceinline__ float4 recipe_cap_fp64(uint64_t seed, uint64_t ctr) {
 
 // Block-level fix-up queue of the fused kernels.  Flagged local indices are
 // collected in shared memory (a warp reserves its slots with one shared-memory
-// atomic) and published to the global queue once per block at the end of the
-// kernel (one global atomic per block).  A global atomic per flagged warp-chunk
+// atomic); the sample kernel recomputes them at the end of the block
+// (block_queue_fix), the reflection kernel publishes them to the global queue
+// with one global atomic per block (block_queue_flush).  A global atomic per flagged warp-chunk
 // instead (round 1) stalled the warp on the ~L2 round trip of its return value
 // in the ~12% of warp-chunks that hold a flagged sample: 8% of the kernel's
 // time at config 4 (tools/fused_ablation.cu).  Samples past the block's slots
@@ -112,6 +113,28 @@ __device__ __forceinline__ void queue_flags(const FixQueue& fq, BlockQueue& bq, 
     }
 }
 
+// Recomputes the block's queued samples in float64 where the block's work
+// ends, all threads of the block busy (all call it once, after their sample
+// loop) -- no second launch for them; samples past the block queue went to
+// the global queue and the fix-up kernel.
+#ifndef VNDF_PHILOX_BLOCK_FIX
+#define VNDF_PHILOX_BLOCK_FIX 1  // 0: publish the block queue to the fix-up kernel (0.9% slower at config 4)
+#endif
+template <int RECIPE>
+__device__ __forceinline__ void block_queue_fix(const FixQueue& fq, BlockQueue& bq, uint64_t seed, uint64_t first,
+                                                float* hx, float* hy, float* hz, float* pdf) {
+    __syncthreads();
+    const unsigned cnt = min(bq.count, fq.bcap);
+    for (unsigned t = threadIdx.x; t < cnt; t += blockDim.x) {
+        const uint64_t k = bq.idx[t];
+        const float4 f = recipe_cap_fp64<RECIPE>(seed, first + k);
+        hx[k] = f.x;
+        hy[k] = f.y;
+        hz[k] = f.z;
+        if (pdf) pdf[k] = f.w;
+    }
+}
+
 // Publishes the block's queue (all threads of the block call it once).
 __device__ __forceinline__ void block_queue_flush(const FixQueue& fq, BlockQueue& bq) {
     __syncthreads();
@@ -124,8 +147,6 @@ __device__ __forceinline__ void block_queue_flush(const FixQueue& fq, BlockQueue
     }
 }
 
-// ctr = first + k, the Philox counter of local sample k; returns the
-// conditioning flag (always false for Heitz)
 // One sample from its two blocks of Philox words; returns the conditioning
 // flag (always false for Heitz).
 template <int METHOD, bool PDF, int RECIPE>
@@ -217,7 +238,7 @@ struct PhiloxLaunch {
 // high word and differ only in the low bits (no 64-bit add per sample).
 template <int METHOD, bool PDF, int V, bool ALIGNED, int RECIPE = kRecipeC4>
 __global__ void __launch_bounds__(PhiloxLaunch<METHOD>::kBlock, PhiloxLaunch<METHOD>::kMinBlocks)
-    philox_kernel(uint64_t first, int64_t n, float* __restrict__ hxp, float* __restrict__ hyp,
+    philox_kernel(uint64_t seed, uint64_t first, int64_t n, float* __restrict__ hxp, float* __restrict__ hyp,
                   float* __restrict__ hzp, float* __restrict__ pdfp, FixQueue fq,
                   const __grid_constant__ PhiloxKeys ks) {
     __shared__ BlockQueue bq;
@@ -269,7 +290,12 @@ __global__ void __launch_bounds__(PhiloxLaunch<METHOD>::kBlock, PhiloxLaunch<MET
             }
         }
     }
-    if (METHOD == kCap) block_queue_flush(fq, bq);
+    if (METHOD == kCap) {
+        if (VNDF_PHILOX_BLOCK_FIX)
+            block_queue_fix<RECIPE>(fq, bq, seed, first, hxp, hyp, hzp, PDF ? pdfp : nullptr);
+        else
+            block_queue_flush(fq, bq);
+    }
 }
 
 // ------------------------------------------- fused Philox reflection (NEXT-2) --

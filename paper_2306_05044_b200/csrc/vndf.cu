@@ -283,8 +283,9 @@ vndf_status launch_stream(const StreamArgs& a, int64_t n, cudaStream_t s) {
 }
 
 // Test hook: VNDF_DEBUG_FIXUP_CAP=k (read once) shrinks the fused kernels'
-// global fix-up queues to k entries, so the overflow path (full rescan) runs;
-// results are bit-identical by design (tests/test_overflow_gpu.py).
+// fix-up queues (global and, unless VNDF_DEBUG_BLOCK_QUEUE is set, per block)
+// to k entries, so the overflow path (full rescan) runs; results are
+// bit-identical by design (tests/test_overflow_gpu.py).
 int64_t debug_fixup_cap() {
     static const int64_t cap = [] {
         const char* v = getenv("VNDF_DEBUG_FIXUP_CAP");
@@ -300,7 +301,8 @@ int64_t debug_fixup_cap() {
 unsigned block_queue_cap() {
     static const unsigned cap = [] {
         const char* v = getenv("VNDF_DEBUG_BLOCK_QUEUE");
-        const long long k = v ? atoll(v) : 0;
+        long long k = v ? atoll(v) : 0;
+        if (k <= 0 && debug_fixup_cap() > 0) k = debug_fixup_cap();  // "every queue shrunk"
         return (unsigned)(k > 0 && k < kBlockQueue ? k : kBlockQueue);
     }();
     return cap;
@@ -354,7 +356,7 @@ vndf_status launch_philox_v(uint64_t seed, uint64_t first, int64_t n, float* hx,
         }
     }
     philox_kernel<METHOD, PDF, V, ALIGNED, RECIPE>
-        <<<grid, block, 0, s>>>(first, n, hx, hy, hz, pdf, fq, philox_keys(seed));
+        <<<grid, block, 0, s>>>(seed, first, n, hx, hy, hz, pdf, fq, philox_keys(seed));
     e = cudaGetLastError();
     if (e == cudaSuccess && METHOD == kCap) {
         // one thread per queue slot up to SMs x 32 blocks; blocks past the
