@@ -248,9 +248,10 @@ int widest_vector(const StreamArgs& a) {
 }
 
 // Small calls (fewer samples than one 8-sample chunk per thread of one
-// 128-thread block per SM) are latency-bound: 4-sample chunks in 64-thread
-// blocks spread them over more SMs and shorten each thread's chain (config 1,
-// 2^16 samples: cap 2.54 -> 1.95 us, Heitz 2.11 -> 1.62 us per launch;
+// 128-thread block per SM) are latency-bound: one sample per thread in
+// 64-thread blocks spreads them over all SMs and gives each thread the
+// shortest chain (config 1, 2^16 samples, per launch: cap 2.47 us at 8 x 128,
+// 1.73 at 4 x 64, 1.49 at 1 x 64; Heitz 2.10, 1.65, 1.45;
 // profiles/r2/stream_fixup_r2.txt).  Explicit vndf_set_launch_config values win.
 bool small_call(int64_t n) {
     int sms = 0;
@@ -274,7 +275,7 @@ vndf_status launch_stream_v(const StreamArgs& a, int64_t n, cudaStream_t s) {
 template <int METHOD, bool PDF>
 vndf_status launch_stream(const StreamArgs& a, int64_t n, cudaStream_t s) {
     int v = widest_vector(a);
-    if (v == 8 && prefs().vector_width == 0 && small_call(n)) v = 4;
+    if (prefs().vector_width == 0 && small_call(n)) v = 1;
     switch (v) {
         case 8: return launch_stream_v<METHOD, PDF, 8>(a, n, s);
         case 4: return launch_stream_v<METHOD, PDF, 4>(a, n, s);
