@@ -9,11 +9,11 @@
 // path (one chunk per thread by default, grid-stride if the grid is capped);
 // the n mod V tail is done by the first threads of the grid with scalar
 // accesses.  A flagged sample is recomputed in float64 at once, in the thread
-// that found it, from the inputs it holds in registers: inlined in the 4-sample
-// loop of small, latency-bound calls (config 1: 1.89 -> 1.72 us per launch, the
-// call's ~80 clocks and the scheduling barrier it puts in the loop gone), an
-// out-of-line call (cap_fp64) in the 8-sample loop (inlined there it measured
-// 3% slower at 2^20 samples).  Round 1 pushed
+// that found it, from the inputs it holds in registers: inlined in the 1- and
+// 4-sample loops that small, latency-bound calls use (config 1 at 4-sample
+// chunks: 1.89 -> 1.72 us per launch, the call's ~80 clocks and the scheduling
+// barrier it puts in the loop gone), an out-of-line call (cap_fp64) in the
+// 8-sample loop (inlined there it measured 3% slower at 2^20 samples).  Round 1 pushed
 // flagged samples to a shared-memory queue, recomputed after a block barrier
 // from a reload of their inputs; inline is faster wherever it was measured
 // (config 5: 7.12 vs 6.86 TB/s; config 1: 2.54 vs 2.81 us per launch -- the
