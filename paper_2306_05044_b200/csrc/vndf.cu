@@ -4,26 +4,28 @@
 // describes each kernel, its roofline and its algorithmic bytes per sample.
 //
 // One translation unit:
-//   vndf_device.cuh      per-sample arithmetic (cap, Heitz, fp64 fix-ups, Philox,
-//                        config-4 generation, reflection, pdf)
+//   vndf_device.cuh      per-sample arithmetic (cap, Heitz, fp64 recomputation,
+//                        Philox, config-4 / config-5 generation, reflection, pdf)
 //   kernels_common.cuh   argument structs, 128/256-bit streaming loads and
-//                        stores, programmatic dependent launch, TMA bulk copy
+//                        stores, programmatic dependent launch, the in-thread
+//                        float64 recomputation
 //   kernels_stream.cuh   stream_kernel<METHOD, PDF, V>: streamed SoA sampling
 //                        (cap, Heitz, native cap), one V-sample chunk per
-//                        thread, block-level float64 fix-up queue
+//                        thread, flagged samples recomputed in the thread
 //   kernels_philox.cuh   philox_kernel<METHOD, PDF, V, ALIGNED, RECIPE>: fused
 //                        Philox4x32-10 generation (config-4 or config-5
-//                        recipe) + sampling + pdf;
-//                        philox_reflect_kernel: the same + reflection, Eq. 20
-//                        pdf and G2/G1 weight (NEXT-2); deferred fix-up queues
-//                        and kernels; raw Philox words; fix-up counters
+//                        recipe) + sampling + pdf, flagged samples recomputed
+//                        at the end of each block; philox_reflect_kernel: the
+//                        same + reflection, Eq. 20 pdf and G2/G1 weight
+//                        (NEXT-2); the fix-up kernels (overflow / reflection);
+//                        raw Philox words; fix-up counters
 //   kernels_next.cuh     pdf_kernel (NEXT-4), reflect_kernel / furnace_kernel
 //                        (NEXT-2), histogram_kernel (NEXT-3), microbench_kernel
 //                        (NEXT-1)
 //   vndf.cu (this file)  launch configuration, argument validation, device
-//                        caches (occupancy, sine table, memory pool, host
-//                        staging), the zero-copy host path, the extern "C"
-//                        entry points
+//                        caches (occupancy, memory pool, host staging), the
+//                        host-buffer paths (zero-copy / DMA staging), the
+//                        extern "C" entry points
 #include <cuda_runtime.h>
 
 #include <algorithm>
