@@ -91,6 +91,22 @@ __global__ void __launch_bounds__(1024, 1) probe(uint32_t seed, long long* cycle
                     asm volatile("fma.rn.f32 %0, %0, 0f3F7FF972, %1;" : "+f"(f[c][k % 4]) : "f"(f[c][(k + 1) % 4]));
             }
             if (MODE == 4) round_hilo(x[c], y[c], z[c], v[c]);
+            if (MODE >= 6) {  // a round plus K instructions of one other type, same warp
+                round(x[c], y[c], z[c], v[c]);
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    if (MODE == 6) asm volatile("mul.rn.f32 %0, %0, %1;" : "+f"(f[c][k % 4]) : "f"(f[c][(k + 1) % 4]));
+                    if (MODE == 7) asm volatile("fma.rn.f32 %0, %0, 0f3F7FF972, %1;" : "+f"(f[c][k % 4]) : "f"(f[c][(k + 1) % 4]));
+                    if (MODE == 8) asm volatile("rsqrt.approx.ftz.f32 %0, %0;" : "+f"(f[c][k % 4]));
+                    if (MODE == 9) asm volatile("lop3.b32 %0, %0, %1, 0x1234567, 0x96;" : "+r"(v[c]) : "r"(y[c]));
+                    if (MODE == 10) {
+                        uint32_t t = __float_as_uint(f[c][k % 4]);
+                        asm volatile("add.u32 %0, %0, %1;" : "+r"(t) : "r"(x[c]));
+                        f[c][k % 4] = __uint_as_float(t);
+                    }
+                    if (MODE == 11) asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(f[c][k % 4]) : "f"(f[c][(k + 1) % 4]), "f"(f[c][(k + 2) % 4]));
+                }
+            }
             if (MODE == 5) {
 #pragma unroll
                 for (int k = 0; k < K; ++k)
@@ -138,6 +154,12 @@ int main() {
     printf("  round | 8 FFMA, split warps %.2f\n", clocks_per_unit<3, 8>(sms, cyc, sink));
     printf("  round as IMAD.HI + IMAD     %.2f\n", clocks_per_unit<4, 0>(sms, cyc, sink));
     printf("  4 FMUL only                %.2f\n", clocks_per_unit<5, 4>(sms, cyc, sink));
+    printf("  round + 4 FMUL             %.2f\n", clocks_per_unit<6, 4>(sms, cyc, sink));
+    printf("  round + 4 FFMA (immediate) %.2f\n", clocks_per_unit<7, 4>(sms, cyc, sink));
+    printf("  round + 4 FFMA (3 regs)    %.2f\n", clocks_per_unit<11, 4>(sms, cyc, sink));
+    printf("  round + 2 MUFU.RSQ         %.2f\n", clocks_per_unit<8, 2>(sms, cyc, sink));
+    printf("  round + 4 LOP3             %.2f\n", clocks_per_unit<9, 4>(sms, cyc, sink));
+    printf("  round + 4 IADD3            %.2f\n", clocks_per_unit<10, 4>(sms, cyc, sink));
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) printf("CUDA error %s\n", cudaGetErrorString(e));
     return 0;
