@@ -33,11 +33,18 @@ for n in (1, 7, 9, 4099, 70001):
         vndf.vndf_sample_cap_philox(3, 2**32 - 5, n, *o)
         vndf.vndf_sample_heitz2018_philox(3, 7, n, *o[:3], None)
         vndf.vndf_count_fixups_philox(3, 0, n, c)
+        vndf.vndf_sample_cap_philox_edge(4, 3, n, *o)
+        vndf.vndf_sample_heitz2018_philox_edge(4, 0, n, *o[:3], None)
+        vndf.vndf_sample_cap_pdf_native(*ins, *outs[:4])
+        r = [torch.zeros(n + 8, device=dev)[off:off + n] for _ in range(5)]
+        vndf.vndf_sample_cap_reflect_philox(3, 1, n, *r)
         w = torch.zeros(4 * n, dtype=torch.int32, device=dev)
         vndf.vndf_philox4x32_10(3, 0, n, 1, w)
     hin = [x[k].cpu().pin_memory() for k in synth.PLANES]
     hout = [torch.zeros(n).pin_memory() for _ in range(4)]
     vndf.vndf_sample_cap_pdf_host(*hin, *hout)
+    vndf.vndf_sample_cap_pdf_host(*hin, *hout[:3], None)
+    vndf.vndf_sample_cap_philox_host(3, 5, n, *hout)
 s = torch.zeros(2, dtype=torch.float64, device=dev)
 vndf.vndf_furnace(0, (0.3, 0.2, 0.9327379), (0.05, 0.3), 1, 100003, s)
 vndf.vndf_furnace(1, (0.3, 0.2, 0.9327379), (0.05, 0.3), 1, 100003, s)
