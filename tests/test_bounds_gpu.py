@@ -36,7 +36,7 @@ def check(bufs, n, off):
         assert not np.any(h[G + off:G + off + n] == 0x7FC0DEAD), "output element not written"
 
 
-@pytest.mark.parametrize("n", [1, 9, 4099, 65541])
+@pytest.mark.parametrize("n", [1, 9, 4099, 65541, (1 << 20) + 3])
 @pytest.mark.parametrize("off", [0, 4, 1])
 def test_guard_bands(env, n, off):
     vndf, synth, dev = env
@@ -54,6 +54,10 @@ def test_guard_bands(env, n, off):
         (4, lambda o: vndf.vndf_sample_cap_philox(3, 2**32 - 3, n, *o)),
         (4, lambda o: vndf.vndf_sample_heitz2018_philox(3, 11, n, *o)),
         (1, lambda o: vndf.vndf_pdf(*ins[:3], *ins[:3], ins[3], ins[4], o[0])),
+        (4, lambda o: vndf.vndf_sample_cap_pdf_native(*ins, *o)),
+        (4, lambda o: vndf.vndf_sample_cap_philox_edge(4, 5, n, *o)),
+        (4, lambda o: vndf.vndf_sample_heitz2018_philox_edge(4, 0, n, *o)),
+        (5, lambda o: vndf.vndf_sample_cap_reflect_philox(3, 2, n, *o)),
     ]
     for k, fn in calls:
         bufs, outs = guarded(n, off, dev, k)
