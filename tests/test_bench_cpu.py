@@ -67,3 +67,21 @@ def test_line_order_and_summary(bench):
     assert s["c4_gsamples_s"] == 147.0 and s["c4_frac_fma_pipe"] == 0.74 and s["c3_gb_s"] == 7200.0
     assert s["c1_cap_us"] == 1.9 and s["c5_t_heitz_over_t_cap"] is None and s["parity_over_tol"] == 0
     assert o["extra"] == 1
+
+
+def test_c5_over_tolerance_counts(bench, orc):
+    """The cpu leg's oracle half of the config-5 robustness object: outputs equal
+    to the oracle's count zero, a perturbed sample counts one."""
+    import synth
+    x = synth.fill_numpy(5, 4, 256)
+    ins = [x[k] for k in synth.PLANES]
+    kept = {"inputs": ins}
+    for name, method in (("cap", orc.CAP), ("heitz", orc.HEITZ)):
+        h, p, _ = orc.batch_sample(method, *ins, pdf=True)
+        kept[name] = [h[0].astype(np.float32), h[1].astype(np.float32), h[2].astype(np.float32),
+                      p.astype(np.float32)]
+    kept["heitz"][0][7] += 1e-3
+    robust = {"cap": {}, "heitz": {}}
+    bench.c5_over_tolerance(robust, kept)
+    assert robust["cap"]["over_tolerance"] == 0 and robust["heitz"]["over_tolerance"] == 1
+    assert robust["cap"]["of_sampled"] == 256
