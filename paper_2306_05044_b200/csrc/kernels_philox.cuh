@@ -13,13 +13,14 @@
 #endif
 
 // ----------------------------------------------------- fused Philox kernel --
-// Deferred float64 fix-up of the fused kernel (compute-bound: an in-thread
-// float64 recomputation diverges the warp -- measured 138 against 147
-// Gsamples/s at config 4, profiles/r2/fused_variants_r2.txt).  Flagged local
-// indices (~0.05% of the config-4 samples) are queued per block (BlockQueue
-// below); a second kernel recomputes them with all lanes busy.  If the global
-// queue overflowed (count > cap), the fix-up kernel rescans every sample's
-// flag instead: always correct, slower only then.
+// Deferred float64 fix-up of the fused kernels (compute-bound: an in-thread
+// float64 recomputation in the sample loop diverges the warp -- measured 138
+// against 147 Gsamples/s at config 4, profiles/r2/fused_variants_r2.txt).
+// Flagged local indices (~0.05% of the config-4 samples) are queued per block
+// (BlockQueue below) and recomputed by the whole block at the end of its
+// sample loop; a block queue's overflow goes to a global queue that the fix-up
+// kernel drains, and if that overflowed too (count > cap) the fix-up kernel
+// rescans every sample's flag: always correct, slower only then.
 
 // Config-4 inputs of Philox counter ctr (both blocks, SURVEY s.8(d)).
 template <bool FW_HI>
@@ -59,10 +60,10 @@ __device__ __forceinline__ float4 recipe_cap_fp64(uint64_t seed, uint64_t ctr) {
 // collected in shared memory (a warp reserves its slots with one shared-memory
 // atomic); the sample kernel recomputes them at the end of the block
 // (block_queue_fix), the reflection kernel publishes them to the global queue
-// with one global atomic per block (block_queue_flush).  A global atomic per flagged warp-chunk
-// instead (round 1) stalled the warp on the ~L2 round trip of its return value
-// in the ~12% of warp-chunks that hold a flagged sample: 8% of the kernel's
-// time at config 4 (tools/fused_ablation.cu).  Samples past the block's slots
+// with one global atomic per block (block_queue_flush).  Round 1's global
+// atomic per flagged warp-chunk stalled the warp on the L2 round trip of its
+// return value in the ~12% of warp-chunks that hold a flagged sample (the
+// shared-memory queue measured +0.9% at config 4).  Samples past the block's slots
 // go to the global queue directly (correct, slower: a persistent block meets
 // ~1.8k flagged samples at 2^30 samples per call, so only calls far larger
 // than config 4 reach it; test hook VNDF_DEBUG_BLOCK_QUEUE).
