@@ -398,7 +398,7 @@ vndf_status launch_philox(uint64_t seed, uint64_t first, int64_t n, float* hx, f
               : launch_philox_v<METHOD, false, PV, false, RECIPE>(seed, first, n, hx, hy, hz, pdf, s);
 }
 
-// Fused Philox reflection (NEXT-2): same grid, table, queue and fix-up
+// Fused Philox reflection (NEXT-2): same grid, queue and fix-up
 // structure as launch_philox_v, five output planes.
 template <int METHOD, int V, bool ALIGNED>
 vndf_status launch_philox_reflect_v(uint64_t seed, uint64_t first, int64_t n, const ReflectOut& out,
