@@ -1,7 +1,8 @@
 /*
  * c_demo.c -- the libvndf C ABI used from plain C (no Python, no torch):
  * sample 2^20 GGX visible normals by the spherical cap (vndf_sample_cap_pdf),
- * then the same through the fused Philox entry point, and print a checksum.
+ * then through the fused Philox entry point, device and host (end to end),
+ * and print a checksum.
  *
  *   gcc -std=c99 -O2 examples/c_demo.c -Iinclude -I/usr/local/cuda/include \
  *       -Lpaper_2306_05044_b200 -lvndf -L/usr/local/cuda/lib64 -lcudart \
@@ -81,6 +82,18 @@ int main(void)
     double zsum = 0.0;
     for (int64_t i = 0; i < n; ++i) zsum += h_out[2][i];
     printf("vndf_sample_cap_philox: mean h.z=%.6f\n", zsum / (double)n);
+
+    /* the same samples end to end into plain malloc'd host memory (the host
+       entry point stages chunks through device memory and copies them back) */
+    float *e_out[4];
+    for (int k = 0; k < 4; ++k) e_out[k] = (float *)malloc(bytes);
+    CHECK(vndf_sample_cap_philox_host(3, 0, n, e_out[0], e_out[1], e_out[2], e_out[3], NULL));
+    int64_t mismatches = 0;
+    for (int64_t i = 0; i < n; ++i) mismatches += e_out[2][i] != h_out[2][i];
+    printf("vndf_sample_cap_philox_host: %lld of %lld h.z differ from the device call\n",
+           (long long)mismatches, (long long)n);
+    for (int k = 0; k < 4; ++k) free(e_out[k]);
+    if (mismatches) return 3;
     printf("status strings: %s / %s, ABI version %d\n", vndf_status_string(VNDF_OK),
            vndf_status_string(VNDF_ERR_INVALID_ARGUMENT), vndf_version());
     for (int k = 0; k < 7; ++k) { cudaFree(d_in[k]); free(h_in[k]); }
