@@ -119,10 +119,10 @@ __device__ __forceinline__ void pdl_launch_dependents() {
 template <int METHOD, bool PDF>
 __device__ __forceinline__ bool sample_one(float wx, float wy, float wz, float ax, float ay, float u1,
                                            float u2, Sample& o) {
-    const float v1 = u1 - 0.5f;  // exact for u1 on the 2^-24 grid and for u1 >= 1/4
-    if (METHOD == kCap) return cap_fp32<PDF>(wx, wy, wz, ax, ay, v1, u2, 1.0f - u2, o);
-    if (METHOD == kCapNative) return cap_fp32<PDF, kFrameNative>(wx, wy, wz, ax, ay, v1, u2, 1.0f - u2, o);
-    heitz_fp32<PDF>(wx, wy, wz, ax, ay, v1, u2, o);
+    const float p1 = phi_reduced(u1);  // u1 - 1/2 exact for u1 on the 2^-24 grid and for u1 >= 1/4
+    if (METHOD == kCap) return cap_fp32<PDF>(wx, wy, wz, ax, ay, p1, u2, 1.0f - u2, o);
+    if (METHOD == kCapNative) return cap_fp32<PDF, kFrameNative>(wx, wy, wz, ax, ay, p1, u2, 1.0f - u2, o);
+    heitz_fp32<PDF>(wx, wy, wz, ax, ay, p1, u2, o);
     return false;
 }
 

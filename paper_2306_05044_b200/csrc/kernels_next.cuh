@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(256) reflect_kernel(ReflectArgs a, int64_t n) 
         for (int j = 0; j < V; ++j) {
             Reflected r;
             // a flagged sample is recomputed in float64 at once from its registers
-            if (cap_reflect_fp32(wx.v[j], wy.v[j], wz.v[j], ax.v[j], ay.v[j], u1.v[j] - 0.5f, u2.v[j],
+            if (cap_reflect_fp32(wx.v[j], wy.v[j], wz.v[j], ax.v[j], ay.v[j], phi_reduced(u1.v[j]), u2.v[j],
                                  1.0f - u2.v[j], r))
                 r = cap_reflect_fp64(wx.v[j], wy.v[j], wz.v[j], ax.v[j], ay.v[j], u1.v[j], u2.v[j]);
             ox.v[j] = r.x;
@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(256) reflect_kernel(ReflectArgs a, int64_t n) 
             const float wx = a.wx[i], wy = a.wy[i], wz = a.wz[i], ax = a.ax[i], ay = a.ay[i], u1 = a.u1[i],
                         u2 = a.u2[i];
             Reflected r;
-            if (cap_reflect_fp32(wx, wy, wz, ax, ay, u1 - 0.5f, u2, 1.0f - u2, r))
+            if (cap_reflect_fp32(wx, wy, wz, ax, ay, phi_reduced(u1), u2, 1.0f - u2, r))
                 r = cap_reflect_fp64(wx, wy, wz, ax, ay, u1, u2);
             a.ox[i] = r.x;
             a.oy[i] = r.y;
@@ -123,15 +123,15 @@ __global__ void __launch_bounds__(256) furnace_kernel(float wx, float wy, float 
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
         const uint4 W = philox_sample(seed, first + (uint64_t)j);
-        const float v1 = fmaf(fw(W.x), 0x1p-24f, -0.5f);
+        const float p1 = phi_reduced_w(fw(W.x));
         const float f2 = fw(W.y);
         Reflected r;
         if (METHOD == kCap) {
-            if (cap_reflect_fp32(wx, wy, wz, ax, ay, v1, f2 * 0x1p-24f, fmaf(f2, -0x1p-24f, 1.0f), r)) {
+            if (cap_reflect_fp32(wx, wy, wz, ax, ay, p1, f2 * 0x1p-24f, fmaf(f2, -0x1p-24f, 1.0f), r)) {
                 r.weight = cap_reflect_weight_fp64(wx, wy, wz, ax, ay, u01d(W.x), u01d(W.y));
             }
         } else {
-            heitz_reflect_fp32(wx, wy, wz, ax, ay, v1, f2 * 0x1p-24f, r);
+            heitz_reflect_fp32(wx, wy, wz, ax, ay, p1, f2 * 0x1p-24f, r);
         }
         s1 += r.weight;
         s2 += (double)r.weight * r.weight;
@@ -211,15 +211,15 @@ __global__ void __launch_bounds__(256) histogram_kernel(int mode, float wx, floa
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
         const uint4 W = philox_sample(seed, first + (uint64_t)j);
-        const float v1 = fmaf(fw(W.x), 0x1p-24f, -0.5f);
+        const float p1 = phi_reduced_w(fw(W.x));
         const float f2 = fw(W.y);
         const float u2 = f2 * 0x1p-24f, q = fmaf(f2, -0x1p-24f, 1.0f);
         Sample o;
         if (METHOD == kHeitz) {
-            heitz_fp32<false>(wx, wy, wz, ax, ay, v1, u2, o);
+            heitz_fp32<false>(wx, wy, wz, ax, ay, p1, u2, o);
         } else {
-            const bool f = native ? cap_fp32<false, kFrameNative>(wx, wy, wz, ax, ay, v1, u2, q, o)
-                                  : cap_fp32<false>(wx, wy, wz, ax, ay, v1, u2, q, o);
+            const bool f = native ? cap_fp32<false, kFrameNative>(wx, wy, wz, ax, ay, p1, u2, q, o)
+                                  : cap_fp32<false>(wx, wy, wz, ax, ay, p1, u2, q, o);
             if (f) {
                 const float4 d = cap_fp64(wx, wy, wz, ax, ay, fw(W.x) * 0x1p-24f, u2, !native);
                 o.x = d.x;
@@ -286,17 +286,17 @@ __global__ void __launch_bounds__(256) microbench_kernel(uint64_t seed, int64_t 
     float acc = 0.0f;
 #pragma unroll 4
     for (int k = 0; k < iters; ++k) {
-        const float v1 = fmaf(fw(x1), 0x1p-24f, -0.5f);
+        const float p1 = phi_reduced_w(fw(x1));
         const float f2 = fw(x2);
         Sample o;
         bool flag = false;
         if (VARIANT == 0) {
-            flag = cap_fp32<false, kFrameUpper>(wx, wy, in.wz, in.ax, in.ay, v1, f2 * 0x1p-24f,
+            flag = cap_fp32<false, kFrameUpper>(wx, wy, in.wz, in.ax, in.ay, p1, f2 * 0x1p-24f,
                                                 fmaf(f2, -0x1p-24f, 1.0f), o);
         } else if (VARIANT == 1) {
-            heitz_fp32<false, false>(wx, wy, in.wz, in.ax, in.ay, v1, f2 * 0x1p-24f, o);
+            heitz_fp32<false, false>(wx, wy, in.wz, in.ax, in.ay, p1, f2 * 0x1p-24f, o);
         } else {
-            cap_literal_fp32(wx, wy, in.wz, in.ax, in.ay, v1, f2 * 0x1p-24f, o);
+            cap_literal_fp32(wx, wy, in.wz, in.ax, in.ay, p1, f2 * 0x1p-24f, o);
         }
         if (TRACE) trace[t * (int64_t)iters + k] = make_float4(o.x, o.y, o.z, flag ? 1.0f : 0.0f);
         acc += o.x + 2.0f * o.y + 3.0f * o.z;

@@ -155,16 +155,16 @@ __device__ __forceinline__ bool sample_words(uint4 X, uint4 Y, Sample& o) {
     if (RECIPE == kRecipeC5) {
         // edge mix: back-side incidence is flipped (reading R4), as in the streamed kernels
         const Inputs in = c5_inputs_fp32(X, Y);
-        if (METHOD == kCap) return cap_fp32<PDF>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o);
-        heitz_fp32<PDF>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, o);
+        if (METHOD == kCap) return cap_fp32<PDF>(in.wx, in.wy, in.wz, in.ax, in.ay, in.p1, in.u2, in.q, o);
+        heitz_fp32<PDF>(in.wx, in.wy, in.wz, in.ax, in.ay, in.p1, in.u2, o);
         return false;
     }
     const Inputs in = c4_inputs_fp32<VNDF_CAP_FW_HI && METHOD == kCap>(X, Y);
     if (METHOD == kCap) {
         // config-4 inputs are on the upper hemisphere (wi.z = 1 - u > 0): no flip
-        return cap_fp32<PDF, kFrameUpper>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o);
+        return cap_fp32<PDF, kFrameUpper>(in.wx, in.wy, in.wz, in.ax, in.ay, in.p1, in.u2, in.q, o);
     }
-    heitz_fp32<PDF, false>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, o);
+    heitz_fp32<PDF, false>(in.wx, in.wy, in.wz, in.ax, in.ay, in.p1, in.u2, o);
     return false;
 }
 
@@ -199,8 +199,8 @@ __global__ void __launch_bounds__(128) philox_fixup_kernel(uint64_t seed, uint64
         const Inputs in = recipe_inputs_seed<RECIPE>(seed, first + k);
         Sample o;
         const bool f = RECIPE == kRecipeC5
-                           ? cap_fp32<true>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o)
-                           : cap_fp32<true, kFrameUpper>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o);
+                           ? cap_fp32<true>(in.wx, in.wy, in.wz, in.ax, in.ay, in.p1, in.u2, in.q, o)
+                           : cap_fp32<true, kFrameUpper>(in.wx, in.wy, in.wz, in.ax, in.ay, in.p1, in.u2, in.q, o);
         if (f) fix(k);
     }
 }
@@ -311,8 +311,8 @@ struct ReflectOut {
 template <int METHOD>
 __device__ __forceinline__ bool philox_reflect_one(const PhiloxKeys& ks, uint64_t ctr, Reflected& r) {
     const Inputs in = c4_inputs_ks<VNDF_CAP_FW_HI && METHOD == kCap>(ks, ctr);
-    if (METHOD == kCap) return cap_reflect_fp32<false>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, r);
-    heitz_reflect_fp32<false>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, r);
+    if (METHOD == kCap) return cap_reflect_fp32<false>(in.wx, in.wy, in.wz, in.ax, in.ay, in.p1, in.u2, in.q, r);
+    heitz_reflect_fp32<false>(in.wx, in.wy, in.wz, in.ax, in.ay, in.p1, in.u2, r);
     return false;
 }
 
@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(128) philox_reflect_fixup_kernel(uint64_t seed
     for (uint64_t k = t0; k < (uint64_t)n; k += stride) {  // overflow: rescan
         const Inputs in = c4_inputs_seed(seed, first + k);
         Reflected r;
-        if (cap_reflect_fp32<false>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, r)) fix(k);
+        if (cap_reflect_fp32<false>(in.wx, in.wy, in.wz, in.ax, in.ay, in.p1, in.u2, in.q, r)) fix(k);
     }
 }
 
@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(256) count_stream_kernel(StreamArgs a, int64_t
         if (i < n) {
             Sample o;
             const float u2 = a.u2[i];
-            flag = cap_fp32<true>(a.wx[i], a.wy[i], a.wz[i], a.ax[i], a.ay[i], a.u1[i] - 0.5f, u2,
+            flag = cap_fp32<true>(a.wx[i], a.wy[i], a.wz[i], a.ax[i], a.ay[i], phi_reduced(a.u1[i]), u2,
                                   1.0f - u2, o);
         }
         warp_count(flag, count);
@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(256) count_philox_kernel(uint64_t seed, uint64
         if (i < n) {
             const Inputs in = c4_inputs_seed(seed, first + (uint64_t)i);
             Sample o;
-            flag = cap_fp32<true, kFrameUpper>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o);
+            flag = cap_fp32<true, kFrameUpper>(in.wx, in.wy, in.wz, in.ax, in.ay, in.p1, in.u2, in.q, o);
         }
         warp_count(flag, count);
     }

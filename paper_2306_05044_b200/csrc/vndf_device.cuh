@@ -71,13 +71,20 @@ __device__ __forceinline__ float ex2_approx(float x) {
 }
 
 // sin(2 pi u), cos(2 pi u) for u in [0, 1): phi = 2 pi u1 (Listing 3,
-// Listing 2).  Callers pass the exactly reduced v = u - 1/2 in
-// [-1/2, 1/2) (exact on the 2^-24 grid of the uniforms, and for u >= 1/4
-// generally), so MUFU.SIN / MUFU.COS run on |2 pi v| <= pi where their
-// absolute error is ~2^-21.4; sin(2 pi u) = -sin(2 pi v), same for cos.
-__device__ __forceinline__ void sincos_2pi_reduced(float v, float* s, float* c) {
+// Listing 2).  The samplers take the reduced angle p = 2 pi v of the
+// exactly reduced v = u - 1/2 in [-1/2, 1/2) (exact on the 2^-24 grid of the
+// uniforms, and for u >= 1/4 generally), so MUFU.SIN / MUFU.COS run on
+// |p| <= pi where their absolute error is ~2^-21.4; sin(2 pi u) = -sin(p),
+// same for cos.  p = fl(fl(2 pi) v), one rounding; from a 24-bit integer f
+// (u = f 2^-24) one FFMA forms the same bits (phi_reduced_w).
+constexpr float k2PiF = 6.28318530717958648f;
+__device__ __forceinline__ float phi_reduced(float u) { return (u - 0.5f) * k2PiF; }
+// fl(2 pi) 2^-24 and fl(2 pi) / 2 are exact, so this is fl(fl(2 pi) (f 2^-24 - 1/2)),
+// the bits of phi_reduced(f 2^-24), in one FFMA instead of an FFMA and an FMUL.
+__device__ __forceinline__ float phi_reduced_w(float f) { return fmaf(f, k2PiF * 0x1p-24f, -0.5f * k2PiF); }
+__device__ __forceinline__ void sincos_reduced(float p, float* s, float* c) {
     float sv, cv;
-    __sincosf(v * 6.28318530717958648f, &sv, &cv);
+    __sincosf(p, &sv, &cv);
     *s = -sv;
     *c = -cv;
 }
@@ -100,7 +107,7 @@ struct Sample {
 //   D_vis = 2 (hs.ws) |m|^3 / (pi a ax ay |hs|^4) = |m|^3 / (pi a ax ay |hs|^2),
 //   m = diag(ax, ay, 1) hs (the unnormalised output).
 // ---------------------------------------------------------------------------
-// v1 = u1 - 1/2 and q = 1 - u2 are passed precomputed (they are free when the
+// p1 = 2 pi (u1 - 1/2) and q = 1 - u2 are passed precomputed (they are free when the
 // uniforms are generated in-kernel from integer words).  FRAME selects the
 // handling of the incidence frame (kFrameFlip / kFrameUpper / kFrameNative).
 // The shared body of the cap kernels: steps (1)-(3) up to the unnormalised
@@ -123,7 +130,7 @@ struct CapCore {
 constexpr int kFrameFlip = 0, kFrameUpper = 1, kFrameNative = 2;
 
 template <int FRAME>
-__device__ __forceinline__ CapCore cap_core(float wx, float wy, float wz, float ax, float ay, float v1,
+__device__ __forceinline__ CapCore cap_core(float wx, float wy, float wz, float ax, float ay, float p1,
                                             float u2, float q) {
     CapCore k;
     k.s = (FRAME == kFrameFlip && wz < 0.0f) ? -1.0f : 1.0f;  // reading R4 (flip)
@@ -142,7 +149,7 @@ __device__ __forceinline__ CapCore cap_core(float wx, float wy, float wz, float 
     const float sin2 = u2 * fmaf(k.hz, k.a, rs2);
     const float st = sqrt_approx(sin2);
     float sp, cp;
-    sincos_2pi_reduced(v1, &sp, &cp);
+    sincos_reduced(p1, &sp, &cp);
     // half vector hs = c + ws, not normalised
     k.hx = fmaf(st, cp, wsx);
     k.hy = fmaf(st, sp, wsy);
@@ -171,8 +178,8 @@ __device__ __forceinline__ bool cap_flag(const CapCore& k, float ax, float ay) {
 
 template <bool PDF, int FRAME = kFrameFlip>
 __device__ __forceinline__ bool cap_fp32(float wx, float wy, float wz, float ax, float ay,
-                                         float v1, float u2, float q, Sample& o) {
-    const CapCore k = cap_core<FRAME>(wx, wy, wz, ax, ay, v1, u2, q);
+                                         float p1, float u2, float q, Sample& o) {
+    const CapCore k = cap_core<FRAME>(wx, wy, wz, ax, ay, p1, u2, q);
     // normalise and flip back
     const float t = k.s * k.invN;
     o.x = k.mx * t;
@@ -202,8 +209,8 @@ struct Reflected {
 
 template <bool FLIP = true>
 __device__ __forceinline__ bool cap_reflect_fp32(float wx, float wy, float wz, float ax, float ay,
-                                                 float v1, float u2, float q, Reflected& o) {
-    const CapCore k = cap_core<FLIP ? kFrameFlip : kFrameUpper>(wx, wy, wz, ax, ay, v1, u2, q);
+                                                 float p1, float u2, float q, Reflected& o) {
+    const CapCore k = cap_core<FLIP ? kFrameFlip : kFrameUpper>(wx, wy, wz, ax, ay, p1, u2, q);
     const float inv_w = rsqrt_approx(fmaf(wx, wx, fmaf(wy, wy, wz * wz)));
     const float L = k.L2 * rsqrt_approx(k.L2) * inv_w;       // |M^-1 w| / |w|
     const float t = k.s * k.invN;
@@ -363,12 +370,12 @@ __device__ __forceinline__ float vndf_pdf_fp32(float hx, float hy, float hz, flo
 // production kernels use cap_fp32 (same cost class, no cancellation).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void cap_literal_fp32(float wx, float wy, float wz, float ax, float ay,
-                                                 float v1, float u2, Sample& o) {
+                                                 float p1, float u2, Sample& o) {
     const float tx = ax * wx, ty = ay * wy;
     const float invL = rsqrt_approx(fmaf(tx, tx, fmaf(ty, ty, wz * wz)));
     const float wsx = tx * invL, wsy = ty * invL, wsz = wz * invL;
     float sp, cp;
-    sincos_2pi_reduced(v1, &sp, &cp);
+    sincos_reduced(p1, &sp, &cp);
     const float z = fmaf(1.0f - u2, 1.0f + wsz, -wsz);
     const float st = sqrt_approx(fminf(fmaxf(fmaf(-z, z, 1.0f), 0.0f), 1.0f));
     const float hx = fmaf(st, cp, wsx), hy = fmaf(st, sp, wsy), hz = z + wsz;
@@ -387,7 +394,7 @@ __device__ __forceinline__ void cap_literal_fp32(float wx, float wy, float wz, f
 // ---------------------------------------------------------------------------
 template <bool PDF, bool FLIP = true>
 __device__ __forceinline__ void heitz_fp32(float wx, float wy, float wz, float ax, float ay,
-                                           float v1, float u2, Sample& o) {
+                                           float p1, float u2, Sample& o) {
     const float s = (FLIP && wz < 0.0f) ? -1.0f : 1.0f;
     const float tx = ax * wx, ty = ay * wy;
     const float L2 = fmaf(tx, tx, fmaf(ty, ty, wz * wz));
@@ -405,7 +412,7 @@ __device__ __forceinline__ void heitz_fp32(float wx, float wy, float wz, float a
     const float w2x = -wsz * w1y, w2y = wsz * w1x, w2z = wsx * w1y - wsy * w1x;
     // parameterization of the cross section
     float sp, cp;
-    sincos_2pi_reduced(v1, &sp, &cp);
+    sincos_reduced(p1, &sp, &cp);
     const float r = sqrt_approx(u2);
     const float t1 = r * cp;
     float t2 = r * sp;
@@ -438,9 +445,9 @@ __device__ __forceinline__ void heitz_fp32(float wx, float wy, float wz, float a
 // pdf_h / (4 w.h) and the same G2/G1 weight.
 template <bool FLIP = true>
 __device__ __forceinline__ void heitz_reflect_fp32(float wx, float wy, float wz, float ax, float ay,
-                                                   float v1, float u2, Reflected& o) {
+                                                   float p1, float u2, Reflected& o) {
     Sample h;
-    heitz_fp32<true, FLIP>(wx, wy, wz, ax, ay, v1, u2, h);
+    heitz_fp32<true, FLIP>(wx, wy, wz, ax, ay, p1, u2, h);
     const float inv_w = rsqrt_approx(fmaf(wx, wx, fmaf(wy, wy, wz * wz)));
     const float ux = wx * inv_w, uy = wy * inv_w, uz = wz * inv_w;
     const float dot = fmaxf(fmaf(ux, h.x, fmaf(uy, h.y, uz * h.z)), 0.0f);
@@ -490,10 +497,11 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
 constexpr float kLog2_100F = 6.64385618977472436f;
 constexpr double kLog2_100D = 6.64385618977472436;
 
-// Inputs of one sample in the form the samplers take: v1 = u1 - 1/2 and
-// q = 1 - u2 (both exact).
+// Inputs of one sample in the form the samplers take: p1 = 2 pi (u1 - 1/2)
+// (sincos_reduced), q = 1 - u2 (exact); v1 = u1 - 1/2 (exact) for the float64
+// recomputation.
 struct Inputs {
-    float wx, wy, wz, ax, ay, v1, u2, q;
+    float wx, wy, wz, ax, ay, v1, p1, u2, q;
 };
 
 // Integer multiply-add / high multiply pinned to IMAD (FMA pipe): left to
@@ -626,7 +634,7 @@ __device__ __forceinline__ Inputs c4_inputs_fp32(uint4 X, uint4 Y) {
     const float fa = fw_t<FW_HI>(X.x);
     const float ua = fa * 0x1p-24f;
     const float z = fmaf(fa, -0x1p-24f, 1.0f);          // 1 - ua, exact
-    const float r = sqrt_approx(ua * (1.0f + z));       // sqrt(ua (2 - ua))
+    const float r = sqrt_approx(fmaf(ua, z, ua));       // sqrt(ua (1 + z)) = sqrt(ua (2 - ua)), one rounding
     float sp, cp;
     sincos_2pi_u24(X.y, &sp, &cp);
     in.wx = r * cp;
@@ -635,7 +643,9 @@ __device__ __forceinline__ Inputs c4_inputs_fp32(uint4 X, uint4 Y) {
     // 0.01 * 100^u = 2^((u - 1) log2 100); u log2 100 = fw (2^-24 log2 100) exactly
     in.ax = ex2_approx(fmaf(fw_t<FW_HI>(X.z), kLog2_100F * 0x1p-24f, -kLog2_100F));
     in.ay = ex2_approx(fmaf(fw_t<FW_HI>(X.w), kLog2_100F * 0x1p-24f, -kLog2_100F));
-    in.v1 = fmaf(fw_t<FW_HI>(Y.x), 0x1p-24f, -0.5f);
+    const float f1 = fw_t<FW_HI>(Y.x);
+    in.v1 = fmaf(f1, 0x1p-24f, -0.5f);
+    in.p1 = phi_reduced_w(f1);
     const float f2 = fw_t<FW_HI>(Y.y);
     in.u2 = f2 * 0x1p-24f;
     in.q = fmaf(f2, -0x1p-24f, 1.0f);
@@ -679,6 +689,7 @@ __device__ __forceinline__ Inputs c5_inputs_fp32(uint4 X, uint4 Y) {
     in.ax = alpha_edge(X.z);
     in.ay = alpha_edge(X.w);
     in.v1 = u1 - 0.5f;  // exact: u1 is on the 2^-24 grid
+    in.p1 = in.v1 * k2PiF;
     in.u2 = u2;
     in.q = 1.0f - u2;
     return in;

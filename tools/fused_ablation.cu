@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(256, 1) abl(uint64_t n, float* hx, float* hy, 
                 continue;
             }
             Sample o;
-            fl |= (unsigned)cap_fp32<true, kFrameUpper>(in.wx, in.wy, in.wz, in.ax, in.ay, in.v1, in.u2, in.q, o);
+            fl |= (unsigned)cap_fp32<true, kFrameUpper>(in.wx, in.wy, in.wz, in.ax, in.ay, in.p1, in.u2, in.q, o);
             ox[j] = o.x;
             oy[j] = o.y;
             oz[j] = o.z;
