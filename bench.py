@@ -548,9 +548,14 @@ CONTRACT_KEYS = ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per
                  "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "clocks", "e2e", "gpu_launches")
 
 
+# The driver keeps the contract keys of the line (parsed) and the last ~3 KB of
+# stdout: the per-config objects that matter go last, the summary at the very end.
+TAIL_KEYS = ("fixups", "c1", "c2", "c5", "c5_fused", "heitz_c4", "c3", "parity")
+
+
 def summary(r):
-    """The per-config headline numbers in one short object, placed right after
-    the contract keys (a record that keeps only the head of the line keeps them)."""
+    """The per-config headline numbers in one short object, the last key of the
+    line (a record that keeps only the tail of stdout keeps them)."""
     def g(*path):
         v = r
         for k in path:
@@ -572,8 +577,9 @@ def summary(r):
 
 def ordered(r):
     out = {k: r[k] for k in CONTRACT_KEYS if k in r}
+    out.update({k: v for k, v in r.items() if k not in out and k not in TAIL_KEYS})
+    out.update({k: r[k] for k in TAIL_KEYS if k in r})
     out["summary"] = summary(r)
-    out.update({k: v for k, v in r.items() if k not in out})
     return out
 
 

@@ -56,13 +56,15 @@ def test_cpu_baseline_is_the_oracle(bench, orc):
 
 
 def test_line_order_and_summary(bench):
-    """The contract keys lead the JSON line, then the per-config summary."""
+    """The contract keys lead the JSON line; the per-config objects and then the
+    summary close it (the driver keeps the line's contract keys and the tail of stdout)."""
     r = {"value": 147.0, "metric": "m", "unit": "u", "roofline": {"frac": 0.65, "fma_pipe": {"frac": 0.74}},
          "c3": {"gb_s": 7200.0, "frac_hbm": 1.1, "t_heitz_over_t_cap": 1.0}, "c1": {"cap_us": 1.9},
          "parity": {"over_tol": 0}, "cpu_baseline": {"value": 0.08}, "extra": 1}
     o = bench.ordered(r)
     keys = list(o)
-    assert keys[:4] == ["metric", "value", "unit", "roofline"] and keys[4] == "summary"
+    assert keys[:4] == ["metric", "value", "unit", "roofline"] and keys[-1] == "summary"
+    assert keys[-4:-1] == ["c1", "c3", "parity"] and keys.index("extra") < keys.index("c1")
     s = o["summary"]
     assert s["c4_gsamples_s"] == 147.0 and s["c4_frac_fma_pipe"] == 0.74 and s["c3_gb_s"] == 7200.0
     assert s["c1_cap_us"] == 1.9 and s["c5_t_heitz_over_t_cap"] is None and s["parity_over_tol"] == 0
