@@ -57,8 +57,8 @@ __device__ __forceinline__ float4 recipe_cap_fp64(uint64_t seed, uint64_t ctr) {
 }
 
 // Block-level fix-up queue of the fused kernels.  Flagged local indices are
-// collected in shared memory (a warp reserves its slots with one shared-memory
-// atomic); the sample kernel recomputes them at the end of the block
+// collected in shared memory (a warp, or in the edge mix each flagged lane,
+// reserves its slots with one shared-memory atomic); the sample kernel recomputes them at the end of the block
 // (block_queue_fix), the reflection kernel publishes them to the global queue
 // with one global atomic per block (block_queue_flush).  Round 1's global
 // atomic per flagged warp-chunk stalled the warp on the L2 round trip of its
