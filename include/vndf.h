@@ -315,11 +315,15 @@ vndf_status vndf_microbench_trace(int method, uint64_t seed, int64_t lanes, int 
                                   float *trace, vndf_stream_t stream);
 
 /* Tuning knobs (process-wide, all threads; 0 = each kernel family's default).
- * Results do not depend on them (test_launch_configurations_bit_identical).
+ * Results do not depend on them (test_launch_configurations_bit_identical,
+ * test_default_shapes_across_sizes).
  *   vector_width in {0, 1, 4, 8}: caps the vector path of the sampling
- *     kernels (1 = scalar accesses; the fused kernels honour 1 only).
+ *     kernels (1 = scalar accesses; the fused kernels honour 1 only).  The
+ *     streamed default depends on the call size, in samples per SM: <= 512
+ *     1 sample per thread x 64 threads, <= 2048 1 x 256, <= 8192 4 x 128,
+ *     else 8 x 128 (latency-bound small calls, HBM-bound large ones).
  *   block_size 0 or 64..256 (multiple of 32): threads per block of the
- *     sampling kernels (defaults: 128 streamed, 256 fused).
+ *     sampling kernels (defaults: as above streamed, 512 fused).
  *   blocks_per_sm: 0 = default grid (streamed: one vector chunk per thread;
  *     fused: persistent, SMs x resident blocks); >= 1 = persistent grid-stride grid
  *     of SMs x min(blocks_per_sm, occupancy) blocks; -1 = one chunk per thread. */

@@ -249,22 +249,40 @@ int widest_vector(const StreamArgs& a) {
     return v;
 }
 
-// Small calls (fewer samples than one 8-sample chunk per thread of one
-// 128-thread block per SM) are latency-bound: one sample per thread in
-// 64-thread blocks spreads them over all SMs and gives each thread the
-// shortest chain (config 1, 2^16 samples, per launch: cap 2.47 us at 8 x 128,
-// 1.73 at 4 x 64, 1.49 at 1 x 64; Heitz 2.10, 1.65, 1.45;
-// profiles/r2/stream_fixup_r2.txt).  Explicit vndf_set_launch_config values win.
-bool small_call(int64_t n) {
+// Default launch shape (samples per thread x block size) of a streamed call of
+// n samples, by samples per SM.  Small and mid-size calls are latency-bound:
+// fewer samples per thread give each thread a shorter chain (and the in-thread
+// float64 recomputation inlined, V <= 4), and ~1k blocks or fewer keep the
+// block launch cost down; large calls are HBM-bound, where 8-sample chunks
+// (256-bit accesses) move the most bytes.  Measured per launch (CUDA-graph
+// replay; tools/c1_shapes.py --log2n, profiles/r2/stream_fixup_r2.txt), cap /
+// Heitz in us against the previous 8 x 128 default:
+//   <=  512 per SM  1 x  64   2^16: 1.45 / 1.45
+//   <= 2048 per SM  1 x 256   2^17: 1.75 / 1.83 (2.40 / 2.42); 2^18: 2.26 / 2.14 (3.20 / 2.97)
+//   <= 8192 per SM  4 x 128   2^19: 3.20 / 2.89 (3.43 / 3.50); 2^20: 4.85 / 4.55 (5.69 / 5.16)
+//   above           8 x 128
+// Explicit vndf_set_launch_config values win.
+struct StreamShape {
+    int v, block;
+};
+
+int sm_count_or_default() {
     int sms = 0;
     if (sm_count(&sms) != cudaSuccess || sms <= 0) sms = 148;
-    return n < (int64_t)8 * 128 * sms;
+    return sms;
+}
+
+StreamShape stream_shape(int64_t n) {
+    const int sms = sm_count_or_default();
+    if (n <= (int64_t)512 * sms) return {1, 64};
+    if (n <= (int64_t)2048 * sms) return {1, 256};
+    if (n <= (int64_t)8192 * sms) return {4, 128};
+    return {8, 128};
 }
 
 template <int METHOD, bool PDF, int V>
-vndf_status launch_stream_v(const StreamArgs& a, int64_t n, cudaStream_t s) {
+vndf_status launch_stream_v(const StreamArgs& a, int64_t n, int block, cudaStream_t s) {
     const void* k = (const void*)stream_kernel<METHOD, PDF, V>;
-    const int block = block_size(small_call(n) && prefs().block_size == 0 ? 64 : 128);
     int grid = 0;
     cudaError_t e = grid_for(k, block, std::max<int64_t>(n / V, 1), &grid, /*persistent=*/false);
     if (e != cudaSuccess) return cuda_fail(e);
@@ -276,12 +294,20 @@ vndf_status launch_stream_v(const StreamArgs& a, int64_t n, cudaStream_t s) {
 
 template <int METHOD, bool PDF>
 vndf_status launch_stream(const StreamArgs& a, int64_t n, cudaStream_t s) {
+    const StreamShape sh = stream_shape(n);
     int v = widest_vector(a);
-    if (prefs().vector_width == 0 && small_call(n)) v = 1;
+    int block = 128;
+    if (prefs().vector_width == 0) {
+        v = std::min(v, sh.v);
+        block = sh.block;
+    } else if (n <= (int64_t)512 * sm_count_or_default()) {
+        block = 64;  // explicit chunk width on a small call
+    }
+    block = block_size(block);
     switch (v) {
-        case 8: return launch_stream_v<METHOD, PDF, 8>(a, n, s);
-        case 4: return launch_stream_v<METHOD, PDF, 4>(a, n, s);
-        default: return launch_stream_v<METHOD, PDF, 1>(a, n, s);
+        case 8: return launch_stream_v<METHOD, PDF, 8>(a, n, block, s);
+        case 4: return launch_stream_v<METHOD, PDF, 4>(a, n, block, s);
+        default: return launch_stream_v<METHOD, PDF, 1>(a, n, block, s);
     }
 }
 

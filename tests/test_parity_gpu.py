@@ -457,3 +457,27 @@ def test_launch_configurations_bit_identical(env, cfg):
         assert torch.equal(a, b)
     for a, b in zip(p0, p1):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("n", [(1 << 16) + 9, (1 << 17) + 3, (1 << 18) + 5, (1 << 19) + 7, (1 << 20) + 1])
+def test_default_shapes_across_sizes(env, n):
+    """The size-dependent default launch shape (1 x 64, 1 x 256, 4 x 128, 8 x 128
+    by samples per SM; vndf.cu stream_shape) on the config-5 edge mix: every
+    sample within tolerance of the float64 oracle, and bit-identical to the
+    8 x 128 shape, cap and Heitz."""
+    oracle, vndf, synth, dev = env
+    x = synth.fill(5, 4, n, device=dev)
+    out = _stream_run(vndf, x, synth.PLANES)
+    heitz = _stream_run(vndf, x, synth.PLANES, kernel="heitz")
+    try:
+        vndf.vndf_set_launch_config(8, 128, 0)
+        ref = _stream_run(vndf, x, synth.PLANES)
+        href = _stream_run(vndf, x, synth.PLANES, kernel="heitz")
+    finally:
+        vndf.vndf_set_launch_config(0, 0, 0)
+    for a, b in zip(list(out) + list(heitz), list(ref) + list(href)):
+        assert torch.equal(a, b)
+    host = _host(x, synth.PLANES)
+    h_ref, p_ref, _ = oracle.batch_sample(oracle.CAP, *host, pdf=True)
+    eh, ep = _errors([o.cpu().numpy() for o in out[:3]], out[3].cpu().numpy(), h_ref, p_ref)
+    assert eh.max() <= TOL_H and ep.max() <= TOL_PDF, (float(eh.max()), float(ep.max()))
