@@ -320,7 +320,7 @@ vndf_status vndf_microbench_trace(int method, uint64_t seed, int64_t lanes, int 
  *   vector_width in {0, 1, 4, 8}: caps the vector path of the sampling
  *     kernels (1 = scalar accesses; the fused kernels honour 1 only).  The
  *     streamed default depends on the call size, in samples per SM: <= 512
- *     1 sample per thread x 64 threads, <= 2048 1 x 256, <= 8192 4 x 128,
+ *     1 sample per thread x 64 threads, <= 2048 1 x 256, <= 262144 4 x 128,
  *     else 8 x 128 (latency-bound small calls, HBM-bound large ones).
  *   block_size 0 or 64..256 (multiple of 32): threads per block of the
  *     sampling kernels (defaults: as above streamed, 512 fused).

@@ -250,17 +250,20 @@ int widest_vector(const StreamArgs& a) {
 }
 
 // Default launch shape (samples per thread x block size) of a streamed call of
-// n samples, by samples per SM.  Small and mid-size calls are latency-bound:
-// fewer samples per thread give each thread a shorter chain (and the in-thread
-// float64 recomputation inlined, V <= 4), and ~1k blocks or fewer keep the
-// block launch cost down; large calls are HBM-bound, where 8-sample chunks
-// (256-bit accesses) move the most bytes.  Measured per launch (CUDA-graph
-// replay; tools/c1_shapes.py --log2n, profiles/r2/stream_fixup_r2.txt), cap /
-// Heitz in us against the previous 8 x 128 default:
-//   <=  512 per SM  1 x  64   2^16: 1.45 / 1.45
-//   <= 2048 per SM  1 x 256   2^17: 1.75 / 1.83 (2.40 / 2.42); 2^18: 2.26 / 2.14 (3.20 / 2.97)
-//   <= 8192 per SM  4 x 128   2^19: 3.20 / 2.89 (3.43 / 3.50); 2^20: 4.85 / 4.55 (5.69 / 5.16)
-//   above           8 x 128
+// n samples, by samples per SM.  Small calls are latency-bound: fewer samples
+// per thread give each thread a shorter chain (and the in-thread float64
+// recomputation inlined, V <= 4), and ~1k blocks or fewer keep the block launch
+// cost down; up to ~2^25 samples 4-sample chunks (80 registers against 124)
+// keep more warps in flight; from 2^26 up 8-sample chunks (256-bit accesses)
+// move the most bytes.  Measured per launch (CUDA-graph replay or back-to-back
+// launches, shapes interleaved; tools/c1_shapes.py --log2n, tools/shape_ab.py,
+// profiles/r2/stream_fixup_r2.txt), cap / Heitz in us against the previous
+// 8 x 128 default:
+//   <=    512 per SM  1 x  64   2^16: 1.45 / 1.45
+//   <=   2048 per SM  1 x 256   2^17: 1.75 / 1.83 (2.40 / 2.42); 2^18: 2.26 / 2.14 (3.20 / 2.97)
+//   <= 262144 per SM  4 x 128   2^20: 5.06 / 4.76 (5.85 / 5.38); 2^22: 24.9 / 24.4 (26.5 / 26.3);
+//                               2^24: 103.7 / 103.8 (106.7 / 106.5)
+//   above             8 x 128   2^26: 417.8 (418.1 at 4 x 128)
 // Explicit vndf_set_launch_config values win.
 struct StreamShape {
     int v, block;
@@ -276,7 +279,7 @@ StreamShape stream_shape(int64_t n) {
     const int sms = sm_count_or_default();
     if (n <= (int64_t)512 * sms) return {1, 64};
     if (n <= (int64_t)2048 * sms) return {1, 256};
-    if (n <= (int64_t)8192 * sms) return {4, 128};
+    if (n <= (int64_t)262144 * sms) return {4, 128};
     return {8, 128};
 }
 

@@ -459,7 +459,7 @@ def test_launch_configurations_bit_identical(env, cfg):
         assert torch.equal(a, b)
 
 
-@pytest.mark.parametrize("n", [(1 << 16) + 9, (1 << 17) + 3, (1 << 18) + 5, (1 << 19) + 7, (1 << 20) + 1])
+@pytest.mark.parametrize("n", [(1 << 16) + 9, (1 << 17) + 3, (1 << 18) + 5, (1 << 19) + 7, (1 << 22) + 1])
 def test_default_shapes_across_sizes(env, n):
     """The size-dependent default launch shape (1 x 64, 1 x 256, 4 x 128, 8 x 128
     by samples per SM; vndf.cu stream_shape) on the config-5 edge mix: every
