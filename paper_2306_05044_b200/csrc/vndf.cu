@@ -938,7 +938,15 @@ vndf_status vndf_sample_cap_reflect(const float* wi_x, const float* wi_y, const 
     for (auto p : out) v = std::min(v, aligned(p, 32) ? 8 : aligned(p, 16) ? 4 : 1);
     if (prefs().vector_width == 1) v = 1;
     if (prefs().vector_width == 4) v = std::min(v, 4);
-    const int block = block_size(128);
+    // default shape by samples per SM: 1 x 256 up to 2048 (latency-bound:
+    // 2^17 2.25 vs 3.48 us at 8 x 128), else 8 x 128 (tools/next_shape_ab.py,
+    // profiles/r2/stream_fixup_r2.txt)
+    int block = 128;
+    if (prefs().vector_width == 0 && n <= (int64_t)2048 * sm_count_or_default()) {
+        v = 1;
+        block = 256;
+    }
+    block = block_size(block);
     int grid = 0;
     cudaError_t e = cudaSuccess;
     cudaStream_t s = (cudaStream_t)stream;
@@ -990,6 +998,10 @@ vndf_status vndf_pdf(const float* h_x, const float* h_y, const float* h_z, const
     for (auto p : in) v = std::min(v, aligned(p, 32) ? 8 : aligned(p, 16) ? 4 : 1);
     if (prefs().vector_width == 1) v = 1;
     if (prefs().vector_width == 4) v = std::min(v, 4);
+    // default 4 x 128 at every size: the 8-sample loop holds 8 input planes x 8
+    // samples (84 registers against 62) and was slower everywhere measured
+    // (2^24: 57.5 vs 71.0 us; tools/next_shape_ab.py, profiles/r2/stream_fixup_r2.txt)
+    if (prefs().vector_width == 0) v = std::min(v, 4);
     const int block = block_size(128);
     int grid = 0;
     cudaError_t e = cudaSuccess;
