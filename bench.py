@@ -352,11 +352,25 @@ def cpu_baseline(check=None, c1_planes=None, c3_planes=None, budget_s: float = 1
 
 # ----------------------------------------------------------------- ours ---
 def _git_sha():
+    """The commit of the sources: from git where there is a checkout, else from
+    the build_info.json that build() wrote beside the library, if it describes
+    these very sources (same source hash)."""
     try:
-        return subprocess.run(["git", "-C", ROOT, "rev-parse", "HEAD"], capture_output=True, text=True,
-                              timeout=5).stdout.strip() or None
+        sha = subprocess.run(["git", "-C", ROOT, "rev-parse", "HEAD"], capture_output=True, text=True,
+                             timeout=5).stdout.strip()
+        if sha:
+            return sha
     except Exception:
-        return None
+        pass
+    try:
+        from paper_2306_05044_b200 import _build
+        with open(_build.BUILD_INFO) as f:
+            info = json.load(f)
+        if info.get("libvndf_source_sha256") == _build.source_hash():
+            return info["git"] + ("-dirty" if info.get("git_dirty") else "")
+    except Exception:
+        pass
+    return None
 
 
 def _sha256(tensors, limit):

@@ -69,7 +69,30 @@ class _FileLock:
         self.f.close()
 
 
+BUILD_INFO = os.path.join(HERE, "build_info.json")
+
+
+def _write_build_info() -> None:
+    """Record the git commit the sources were built from (build_info.json,
+    git-ignored, travels with the in-tree .so): the GPU box has no .git, so
+    bench.py reads the commit from here when `git` cannot.  Written only where
+    git answers, never overwritten with an unknown commit."""
+    import json
+    try:
+        r = subprocess.run(["git", "-C", ROOT, "rev-parse", "HEAD"], capture_output=True, text=True, timeout=5)
+        sha = r.stdout.strip()
+        if r.returncode != 0 or not sha:
+            return
+        d = subprocess.run(["git", "-C", ROOT, "status", "--porcelain", "--untracked-files=no"],
+                           capture_output=True, text=True, timeout=5).stdout.strip()
+    except Exception:
+        return
+    with open(BUILD_INFO, "w") as f:
+        json.dump({"git": sha, "git_dirty": bool(d), "libvndf_source_sha256": source_hash()}, f)
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    _write_build_info()
     if not (force or stale()):
         return LIB
     with _FileLock(LIB + ".lock"):
