@@ -119,6 +119,31 @@ def _rand_dir_upper(rng):
     return v / np.linalg.norm(v)
 
 
+def test_G1_smith_form_and_chi_plus(orc):
+    """Eq. 16-17: G1(wm, wi) equals Heitz 2014's Smith masking
+    1/(1 + Lambda(wi)) for every front-facing microfacet (wi.wm > 0, the same
+    sign in std space since (M^-1 wi).(M^T wm) = wi.wm) and is 0 for
+    back-facing ones (the chi+ factor)."""
+    rng = np.random.default_rng(1617)
+    front = back = 0
+    for _ in range(400):
+        ax, ay = np.exp(rng.uniform(np.log(0.01), 0.0, 2))
+        wi = rng.normal(size=3)
+        wi[2] = abs(wi[2]) + 1e-3
+        wi /= np.linalg.norm(wi)
+        wm = rng.normal(size=3)
+        wm[2] = abs(wm[2]) + 1e-3
+        wm /= np.linalg.norm(wm)
+        g = orc.G1(wm, wi, ax, ay)
+        if float(np.dot(wi, wm)) > 1e-9:
+            assert g == pytest.approx(_textbook_G1(wi, ax, ay), rel=1e-9, abs=1e-12)
+            front += 1
+        elif float(np.dot(wi, wm)) < -1e-9:
+            assert g == 0.0
+            back += 1
+    assert front > 50 and back > 50
+
+
 def test_pdf_three_forms_agree(orc):
     """Eq. 1 == G1 max(0,wi.h) D / wi.z via Eq. 12 + Eq. 16-17
     == the textbook Smith/Lambda + theta/phi GGX forms (Heitz 2014)."""
