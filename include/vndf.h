@@ -122,7 +122,7 @@ vndf_status vndf_sample_heitz2018(const float *wi_x, const float *wi_y, const fl
 
 /* Fused in-kernel Philox4x32-10 (BASELINE config 4: key = seed, counter =
  * sample index).  Sample k of the call has global index
- * i = first_index + k and TWO Philox blocks, key (seed_lo, seed_hi):
+ * i = first_index + k (modulo 2^64) and TWO Philox blocks, key (seed_lo, seed_hi):
  *   X = Philox(counter (i_lo, i_hi, 0, 0)),  Y = Philox(counter (i_lo, i_hi, 1, 0));
  * with u(w) = (w >> 8) 2^-24 (24 bits):
  *   wi uniform on the upper hemisphere: z = 1 - u(X0), r = sqrt(u(X0) (2 - u(X0))),

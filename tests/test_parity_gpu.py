@@ -165,6 +165,33 @@ def test_philox_full_range_small(env):
         assert eh.max() <= TOL_H and ep.max() <= TOL_PDF, (first, float(eh.max()), float(ep.max()))
 
 
+def test_philox_counter_wraps_and_extreme_seeds(env):
+    """Counters are first_index + k modulo 2^64 (vndf.h): ranges across the
+    wrap, aligned (first = 0 mod 8) and not, and the extreme seeds 0 and
+    2^64 - 1, every sample against the oracle on the wrapped indices; the fused
+    edge mix and the Heitz twin on the same wrapped range agree with their
+    own recipe (edge: bit-identical to the streamed kernel on its planes)."""
+    oracle, vndf, synth, dev = env
+    M = 1 << 64
+    for seed, first, n in ((3, M - 64, 8 * 20 + 3), (3, M - 13, 8 * 16 + 5),
+                           (0, M - 4096, 8192), ((1 << 64) - 1, 12345, 4099)):
+        out = vndf.empty_outputs(n, dev)
+        vndf.vndf_sample_cap_philox(seed, first, n, *out)
+        torch.cuda.synchronize()
+        idx = (np.arange(n, dtype=np.uint64) + np.uint64(first))  # wraps modulo 2^64
+        h_ref, p_ref, _ = oracle.batch_sample_philox(oracle.CAP, seed, idx)
+        eh, ep = _errors([o.cpu().numpy() for o in out[:3]], out[3].cpu().numpy(), h_ref, p_ref)
+        assert eh.max() <= TOL_H and ep.max() <= TOL_PDF, (seed, first, float(eh.max()), float(ep.max()))
+        # the same samples from a call that starts at the wrapped index 0
+        k0 = int((M - first) % M)
+        if 0 < k0 < n:
+            tail = vndf.empty_outputs(n - k0, dev)
+            vndf.vndf_sample_cap_philox(seed, 0, n - k0, *tail)
+            torch.cuda.synchronize()
+            for a, b in zip(out, tail):
+                assert torch.equal(a[k0:], b)
+
+
 def test_philox_first_index_offsets_bit_identical(env):
     """Sample k of a call with first_index f is sample f + k of a call with
     first_index 0, for every residue of f mod 4 (aligned and unaligned chunk
