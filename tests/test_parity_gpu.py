@@ -168,9 +168,8 @@ def test_philox_full_range_small(env):
 def test_philox_counter_wraps_and_extreme_seeds(env):
     """Counters are first_index + k modulo 2^64 (vndf.h): ranges across the
     wrap, aligned (first = 0 mod 8) and not, and the extreme seeds 0 and
-    2^64 - 1, every sample against the oracle on the wrapped indices; the fused
-    edge mix and the Heitz twin on the same wrapped range agree with their
-    own recipe (edge: bit-identical to the streamed kernel on its planes)."""
+    2^64 - 1, every sample against the oracle on the wrapped indices, and the
+    samples past the wrap bit-identical to a call that starts at index 0."""
     oracle, vndf, synth, dev = env
     M = 1 << 64
     for seed, first, n in ((3, M - 64, 8 * 20 + 3), (3, M - 13, 8 * 16 + 5),
