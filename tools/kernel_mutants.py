@@ -52,10 +52,22 @@ MUTANTS = [
      "in.p1 = phi_reduced_w(f1);", "in.p1 = -phi_reduced_w(f1);"),
     ("streamed tail: h.x written from h.y", "kernels_stream.cuh",
      "            a.hx[i] = o.x;", "            a.hx[i] = o.y;"),
+    ("standalone pdf: |h|^2 for |h|^3", "vndf_device.cuh",
+     "const float h3 = h2 * (h2 * rsqrt_approx(h2));", "const float h3 = h2;"),
+    ("native frame: 1 + ws.z below the horizon taken as 1 - ws.z", "vndf_device.cuh",
+     "rs2 * rcp_approx(1.0f - wsz) : 1.0f + wsz;", "rs2 * rcp_approx(1.0f + wsz) : 1.0f + wsz;"),
+    ("reflection weight: z_i dropped from G2/G1", "vndf_device.cuh",
+     "    const float Lo = sqrt_approx(fmaf(ax * o.x, ax * o.x, fmaf(ay * o.y, ay * o.y, o.z * o.z)));\n    const float wgt = zo * (zi + L) * rcp_approx(fmaf(L, zo, Lo * zi));\n    o.weight = zo > 0.0f ? wgt : 0.0f;\n    return cap_flag",
+     "    const float Lo = sqrt_approx(fmaf(ax * o.x, ax * o.x, fmaf(ay * o.y, ay * o.y, o.z * o.z)));\n    const float wgt = zo * L * rcp_approx(fmaf(L, zo, Lo * zi));\n    o.weight = zo > 0.0f ? wgt : 0.0f;\n    return cap_flag"),
+    ("config-5 inputs: u2 = 0 injection lost", "vndf_device.cuh",
+     "if (((Y.w >> 6) & 0x3Fu) == 0u) u2 = 0.0f;", "if (((Y.w >> 6) & 0x3Fu) == 0u) u2 = 0.5f;"),
+    ("host path: every chunk from the call's first index", "vndf.cu",
+     "result = launch_philox<kCap>(seed, first_index + (uint64_t)off, m,", "result = launch_philox<kCap>(seed, first_index, m,"),
 ]
 
 TESTS = ["tests/test_parity_gpu.py", "tests/test_edge_gpu.py", "tests/test_edge_fused_gpu.py",
-         "tests/test_reflect_gpu.py", "tests/test_pdf_gpu.py", "tests/test_microbench_gpu.py"]
+         "tests/test_reflect_gpu.py", "tests/test_pdf_gpu.py", "tests/test_microbench_gpu.py",
+         "tests/test_native_gpu.py", "tests/test_host_paths_gpu.py"]
 
 
 def build():
